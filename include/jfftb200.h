@@ -1,0 +1,147 @@
+/*
+ * jfftb200.h -- C ABI of libjfftb200.so, the B200-native (sm_100a) J-FFT PCG
+ * hot path (arXiv 2508.02613).
+ *
+ * The reference (/root/reference/pkg/src/jfft) is pure Python on NumPy and has
+ * no FFI of its own; its "operator API" is the set of module-level functions
+ * re-exported by jfft/__init__.py:5-21.  Each entry point below replaces one
+ * of those functions (cited per declaration).  The Python host layer
+ * paper_2508_02613_b200/ binds this ABI with ctypes and keeps the reference's
+ * call signatures; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Plain C types only: pointers + sizes, no torch/CUDA types in signatures
+ *    (streams are passed as void*).
+ *  - Every function returns an int status (JFFTB_OK = 0).  On failure a
+ *    thread-local message is available from jfftb_last_error().  No C++
+ *    exception crosses the boundary.
+ *  - Array arguments are float64, C order, last index contiguous:
+ *      scalar (pixel) field  n0 x ... x n_{d-1}
+ *      vector field          d x n0 x ... x n_{d-1}
+ *      quadrature field      M x d! x n0 x ...   (M = 3 in 2-D, 6 in 3-D)
+ *      half spectrum         d x n0 x ... x (n_{d-1}/2+1) complex (re,im interleaved)
+ *  - `where` selects the memory space of every array argument of that call:
+ *    JFFTB_HOST (pageable or pinned host memory; the call copies and
+ *    synchronises) or JFFTB_DEVICE (device pointers on the grid's device;
+ *    the call is asynchronous on the grid's stream unless stated).
+ *  - Handles are not thread-safe; use one grid handle per calling thread.
+ */
+#ifndef JFFTB200_H
+#define JFFTB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (mapped by the host layer to the reference's exceptions) */
+#define JFFTB_OK          0  /* success */
+#define JFFTB_EINVAL      1  /* invalid argument         -> ValueError       */
+#define JFFTB_ENONFINITE  2  /* NaN/Inf in the recurrence -> SolverAbortError */
+#define JFFTB_ECURVATURE  3  /* curvature <= 0            -> SolverAbortError */
+#define JFFTB_ECUDA       4  /* CUDA / cuFFT failure      -> RuntimeError     */
+
+#define JFFTB_HOST   0
+#define JFFTB_DEVICE 1
+
+/* preconditioner kinds, preconditioners.py:22 PRECONDITIONER_KINDS order */
+#define JFFTB_PC_NONE          0
+#define JFFTB_PC_GREEN         1
+#define JFFTB_PC_JACOBI        2
+#define JFFTB_PC_GREEN_JACOBI  3
+
+/* SolveReport.terminated, solver.py:32-33 */
+#define JFFTB_CONVERGED      0
+#define JFFTB_ITERATION_CAP  1
+
+typedef struct jfftb_grid   jfftb_grid;    /* grid.py:34 Grid (+ device, stream, FFT plans) */
+typedef struct jfftb_op     jfftb_op;      /* operators.py:15 SystemOperator               */
+typedef struct jfftb_green  jfftb_green;   /* preconditioners.py:29 GreenOperator          */
+typedef struct jfftb_jacobi jfftb_jacobi;  /* preconditioners.py:38 JacobiDiagonal         */
+
+/* ---- library ---------------------------------------------------------- */
+const char* jfftb_last_error(void);
+int jfftb_version(void);                   /* 100 * major + minor */
+/* number of kernel launches issued by this thread since the last reset */
+int64_t jfftb_launch_count(int reset);
+
+/* ---- grid / context (grid.py:34-96 make_grid) -------------------------- */
+/* d in {2,3}; n[d] nodes per axis (>= 2); lengths[d] > 0; CUDA device id. */
+int jfftb_grid_create(int d, const int64_t* n, const double* lengths, int device,
+                      jfftb_grid** out);
+int jfftb_grid_destroy(jfftb_grid* g);
+/* run all subsequent work of this grid (and its ops/greens/jacobis) on
+ * `stream` (a cudaStream_t); NULL selects the grid's own stream. */
+int jfftb_grid_set_stream(jfftb_grid* g, void* stream);
+int jfftb_grid_synchronize(jfftb_grid* g);
+
+/* ---- FFT contract (grid.py:200-215 fft_forward / fft_inverse) ---------- */
+int jfftb_fft_forward(jfftb_grid* g, const double* u, double* spec, int where);
+int jfftb_fft_inverse(jfftb_grid* g, const double* spec, double* u, int where);
+
+/* ---- system operator (operators.py:38-101) ----------------------------- */
+/* make_operator (operators.py:38): density rho >= 0 (EINVAL otherwise),
+ * isotropic material (material.py:25) lambda0, mu0. */
+int jfftb_op_create(jfftb_grid* g, const double* rho, int where, double lambda0,
+                    double mu0, jfftb_op** out);
+int jfftb_op_destroy(jfftb_op* op);
+/* apply_system (operators.py:51): out = K(rho) u */
+int jfftb_apply_system(jfftb_op* op, const double* u, double* out, int where);
+/* assemble_rhs (operators.py:61): out = -B^T W rho C0 E; eps_bar is a host
+ * Mandel vector (3 or 6 entries, finite). */
+int jfftb_assemble_rhs(jfftb_op* op, const double* eps_bar, double* out, int where);
+/* total_strain (operators.py:79): quadrature field E + B u */
+int jfftb_total_strain(jfftb_op* op, const double* u, const double* eps_bar,
+                       double* out, int where);
+/* residual_force (operators.py:86): -B^T W sigma(rho, E + B u) */
+int jfftb_residual_force(jfftb_op* op, const double* u, const double* eps_bar,
+                         double* out, int where);
+/* homogenized_stress (operators.py:98): sigma_out (host, 3 or 6 entries) */
+int jfftb_homogenized_stress(jfftb_op* op, const double* u, const double* eps_bar,
+                             double* sigma_out, int where);
+
+/* ---- Green operator (preconditioners.py:50-94) ------------------------- */
+/* assemble_green (preconditioners.py:50): impulse responses of K_ref ->
+ * spectrum -> Hermitised per-frequency pseudo-inverse (cutoff 1e-12 lambda_max),
+ * zero-frequency block = 0.  EINVAL if C_ref is not positive definite. */
+int jfftb_green_create(jfftb_grid* g, double lambda_ref, double mu_ref,
+                       jfftb_green** out);
+int jfftb_green_destroy(jfftb_green* green);
+/* GreenOperator.blocks: host array (n0, ..., n_{d-1}/2+1, d, d) complex */
+int jfftb_green_export_blocks(jfftb_green* green, double* out);
+/* apply_green (preconditioners.py:83) */
+int jfftb_apply_green(jfftb_green* green, const double* r, double* out, int where);
+
+/* ---- Jacobi diagonal (preconditioners.py:97-136) ----------------------- */
+/* assemble_jacobi (preconditioners.py:97): d * 2^d comb probes of K;
+ * EINVAL for odd n or a negative / non-finite probed diagonal. */
+int jfftb_jacobi_create(jfftb_op* op, jfftb_jacobi** out);
+int jfftb_jacobi_destroy(jfftb_jacobi* jac);
+/* JacobiDiagonal.inv_sqrt (vector field layout) */
+int jfftb_jacobi_export(jfftb_jacobi* jac, double* out, int where);
+
+/* Preconditioner.apply (preconditioners.py:156-163) for every kind;
+ * kind = JFFTB_PC_*; green / jac may be NULL when the kind does not use them
+ * (apply_jacobi_half is exposed as kind = -1). */
+int jfftb_apply_precond(int kind, jfftb_green* green, jfftb_jacobi* jac,
+                        const double* r, double* out, int where);
+
+/* ---- PCG (solver.py:64-140) -------------------------------------------- */
+/* pcg(op, rhs, preconditioner, green, eta, max_iter).  `green_pc` is the
+ * preconditioner's Green operator (kinds green / green-jacobi), `jac` its
+ * Jacobi diagonal (jacobi / green-jacobi), `green_term` the Green operator of
+ * the termination functional <r, G r>.  Outputs: x_out (solution, mean
+ * subtracted, in `where` space), history_out (HOST, max_iter + 1 doubles;
+ * entries 0..iterations valid), iterations, terminated (JFFTB_CONVERGED /
+ * JFFTB_ITERATION_CAP), wall_s (host wall time of the call).  Returns
+ * JFFTB_ENONFINITE / JFFTB_ECURVATURE like SolverAbortError. */
+int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
+              jfftb_green* green_term, const double* rhs, int where, double eta,
+              int max_iter, double* x_out, double* history_out, int* iterations,
+              int* terminated, double* wall_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JFFTB200_H */

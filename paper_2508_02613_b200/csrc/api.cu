@@ -1,0 +1,767 @@
+// C ABI of libjfftb200.so (include/jfftb200.h): handle lifetime, host/device
+// staging, preconditioner setup, and the PCG driver loop.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace jfftb {
+
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int64_t g_launches = 0;
+
+// RAII device buffer on a stream
+struct DevBuf {
+  void* ptr = nullptr;
+  DevBuf() = default;
+  explicit DevBuf(size_t bytes) { reset(bytes); }
+  void reset(size_t bytes) {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    if (bytes) JF_CUDA(cudaMalloc(&ptr, bytes));
+  }
+  ~DevBuf() {
+    if (ptr) cudaFree(ptr);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) JF_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return JFFTB_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return JFFTB_ECUDA;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return JFFTB_ECUDA;
+  }
+}
+
+// Stage an input array onto the device: device pointers pass through, host
+// arrays are copied into `tmp`.
+const double* stage_in(jfftb_grid* g, const double* src, size_t count, int where, DevBuf& tmp) {
+  require(src != nullptr, "null input array");
+  if (where == JFFTB_DEVICE) return src;
+  require(where == JFFTB_HOST, "where must be JFFTB_HOST or JFFTB_DEVICE");
+  tmp.reset(count * sizeof(double));
+  JF_CUDA(cudaMemcpyAsync(tmp.ptr, src, count * sizeof(double), cudaMemcpyHostToDevice,
+                          g->stream));
+  return tmp.as<double>();
+}
+double* stage_out(double* dst, size_t count, int where, DevBuf& tmp) {
+  require(dst != nullptr, "null output array");
+  if (where == JFFTB_DEVICE) return dst;
+  require(where == JFFTB_HOST, "where must be JFFTB_HOST or JFFTB_DEVICE");
+  tmp.reset(count * sizeof(double));
+  return tmp.as<double>();
+}
+void finish_out(jfftb_grid* g, double* dst, const double* dev, size_t count, int where) {
+  if (where == JFFTB_HOST) {
+    JF_CUDA(cudaMemcpyAsync(dst, dev, count * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+  }
+}
+
+double* ensure_partials(jfftb_grid* g, int count) {
+  if (g->partials_cap < count) {
+    if (g->partials) JF_CUDA(cudaFree(g->partials));
+    JF_CUDA(cudaMalloc(&g->partials, sizeof(double) * count));
+    g->partials_cap = count;
+  }
+  return g->partials;
+}
+
+void ensure_plans(jfftb_grid* g) {
+  if (g->plans_ready) return;
+  const Geom& geo = g->geo;
+  long long n[3] = {geo.n[0], geo.n[1], geo.n[2]};
+  size_t w1 = 0, w2 = 0, w3 = 0;
+  JF_CUFFT(cufftCreate(&g->plan_fwd_d));
+  JF_CUFFT(cufftCreate(&g->plan_inv_d));
+  JF_CUFFT(cufftCreate(&g->plan_fwd_2d));
+  for (cufftHandle h : {g->plan_fwd_d, g->plan_inv_d, g->plan_fwd_2d})
+    JF_CUFFT(cufftSetAutoAllocation(h, 0));
+  JF_CUFFT(cufftMakePlanMany64(g->plan_fwd_d, geo.d, n, nullptr, 1, geo.N, nullptr, 1, geo.Nh,
+                               CUFFT_D2Z, geo.d, &w1));
+  JF_CUFFT(cufftMakePlanMany64(g->plan_inv_d, geo.d, n, nullptr, 1, geo.Nh, nullptr, 1, geo.N,
+                               CUFFT_Z2D, geo.d, &w2));
+  JF_CUFFT(cufftMakePlanMany64(g->plan_fwd_2d, geo.d, n, nullptr, 1, geo.N, nullptr, 1, geo.Nh,
+                               CUFFT_D2Z, 2 * geo.d, &w3));
+  g->fft_work_bytes = std::max(std::max(w1, w2), w3);
+  if (g->fft_work_bytes) JF_CUDA(cudaMalloc(&g->fft_work, g->fft_work_bytes));
+  for (cufftHandle h : {g->plan_fwd_d, g->plan_inv_d, g->plan_fwd_2d})
+    JF_CUFFT(cufftSetWorkArea(h, g->fft_work));
+  g->plans_ready = true;
+}
+
+__global__ void scale_kernel(double* x, double a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= a;
+}
+
+__global__ void check_rho_kernel(const double* rho, int64_t n, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!(rho[i] >= 0.0)) *bad = 1;  // negative or NaN
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi probing (preconditioners.py:97-119)
+// ---------------------------------------------------------------------------
+__global__ void comb_kernel(double* __restrict__ comb, Geom g, int alpha, int offs) {
+  // comb = 0 except ones on component alpha at nodes with i_a % 2 == o_a
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.d * g.N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int comp = (int)(i / g.N);
+    int64_t rem = i % g.N;
+    bool on = comp == alpha;
+    for (int a = g.d - 1; a >= 0; --a) {
+      const int ia = (int)(rem % g.n[a]);
+      rem /= g.n[a];
+      on = on && ((ia & 1) == ((offs >> a) & 1));
+    }
+    comb[i] = on ? 1.0 : 0.0;
+  }
+}
+__global__ void comb_extract_kernel(double* __restrict__ diag, const double* __restrict__ resp,
+                                    Geom g, int alpha, int offs) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.N;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = v;
+    bool on = true;
+    for (int a = g.d - 1; a >= 0; --a) {
+      const int ia = (int)(rem % g.n[a]);
+      rem /= g.n[a];
+      on = on && ((ia & 1) == ((offs >> a) & 1));
+    }
+    if (on) diag[alpha * g.N + v] = resp[alpha * g.N + v];
+  }
+}
+__global__ void jacobi_finish_kernel(double* __restrict__ diag, int64_t n, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = diag[i];
+    if (!(v >= 0.0) || !isfinite(v)) *bad = 1;
+    if (v == 0.0) v = 1.0;
+    diag[i] = 1.0 / sqrt(v);
+  }
+}
+
+int nblk(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+}
+
+int read_flag(jfftb_grid* g, int* dflag) {
+  int h = 0;
+  JF_CUDA(cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+  JF_CUDA(cudaStreamSynchronize(g->stream));
+  return h;
+}
+
+// precondition r (device, d*N) into out (device) for kind (-1 = jacobi half)
+void precond_device(int kind, jfftb_green* green, jfftb_jacobi* jac, jfftb_grid* g,
+                    const double* r, double* out) {
+  const Geom& geo = g->geo;
+  const int64_t n = geo.d * geo.N;
+  cudaStream_t s = g->stream;
+  auto need_jac = [&]() { require(jac != nullptr, "kind needs an assembled Jacobi diagonal"); };
+  auto need_green = [&]() { require(green != nullptr, "kind needs an assembled Green operator"); };
+  if (kind == JFFTB_PC_NONE) {
+    launch_copy(s, out, r, n);
+  } else if (kind == -1) {
+    need_jac();
+    launch_mul(s, out, jac->inv_sqrt, r, n);
+  } else if (kind == JFFTB_PC_JACOBI) {
+    need_jac();
+    launch_mul2(s, out, jac->inv_sqrt, r, n);
+  } else if (kind == JFFTB_PC_GREEN || kind == JFFTB_PC_GREEN_JACOBI) {
+    need_green();
+    if (kind == JFFTB_PC_GREEN_JACOBI) need_jac();
+    ensure_plans(g);
+    DevBuf spec(sizeof(double2) * geo.d * geo.Nh);
+    DevBuf tmp(kind == JFFTB_PC_GREEN_JACOBI ? sizeof(double) * n : 0);
+    const double* src = r;
+    if (kind == JFFTB_PC_GREEN_JACOBI) {
+      launch_mul(s, tmp.as<double>(), jac->inv_sqrt, r, n);
+      src = tmp.as<double>();
+    }
+    JF_CUFFT(cufftSetStream(g->plan_fwd_d, s));
+    JF_CUFFT(cufftExecD2Z(g->plan_fwd_d, const_cast<double*>(src), spec.as<cufftDoubleComplex>()));
+    launch_green_apply(geo, s, green->blocks, spec.as<double2>(), spec.as<double2>(), 1);
+    JF_CUFFT(cufftSetStream(g->plan_inv_d, s));
+    JF_CUFFT(cufftExecZ2D(g->plan_inv_d, spec.as<cufftDoubleComplex>(), out));
+    if (kind == JFFTB_PC_GREEN_JACOBI) launch_mul(s, out, jac->inv_sqrt, out, n);
+    JF_CUDA(cudaStreamSynchronize(s));  // spec/tmp are freed on return
+  } else {
+    require(false, "unknown preconditioner kind");
+  }
+}
+
+}  // namespace
+
+void set_last_error(const std::string& m) { g_last_error = m; }
+void count_launch(int n) { g_launches += n; }
+
+}  // namespace jfftb
+
+using namespace jfftb;
+
+extern "C" {
+
+const char* jfftb_last_error(void) { return g_last_error.c_str(); }
+int jfftb_version(void) { return 100; }
+int64_t jfftb_launch_count(int reset) {
+  const int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+int jfftb_grid_create(int d, const int64_t* n, const double* lengths, int device,
+                      jfftb_grid** out) {
+  return guarded([&] {
+    require(out != nullptr && n != nullptr && lengths != nullptr, "null argument");
+    require(d == 2 || d == 3, "only d = 2 and d = 3 are supported");
+    int ndev = 0;
+    JF_CUDA(cudaGetDeviceCount(&ndev));
+    require(device >= 0 && device < ndev, "invalid CUDA device");
+    Geom geo{};
+    geo.d = d;
+    geo.N = 1;
+    for (int a = 0; a < 3; ++a) geo.n[a] = 1;
+    for (int a = 0; a < d; ++a) {
+      require(n[a] >= 2 && n[a] < (1 << 20), "grid needs n >= 2 nodes per direction");
+      require(lengths[a] > 0.0 && std::isfinite(lengths[a]), "cell side lengths must be positive");
+      geo.n[a] = (int)n[a];
+      geo.N *= n[a];
+      geo.h[a] = lengths[a] / (double)n[a];
+      geo.hinv[a] = 1.0 / geo.h[a];
+    }
+    geo.nh = geo.n[d - 1] / 2 + 1;
+    geo.Nh = geo.N / geo.n[d - 1] * geo.nh;
+    double vol = 1.0;
+    for (int a = 0; a < d; ++a) vol *= geo.h[a];
+    geo.w = vol / (d == 2 ? 2.0 : 6.0);
+    geo.iso = true;
+    for (int a = 1; a < d; ++a) geo.iso = geo.iso && geo.h[a] == geo.h[0];
+    DeviceGuard dg(device);
+    auto* g = new jfftb_grid();
+    g->geo = geo;
+    g->device = device;
+    if (cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete g;
+      throw Error(JFFTB_ECUDA, "cudaStreamCreate failed");
+    }
+    g->stream = g->own_stream;
+    JF_CUDA(cudaMalloc(&g->dscal, 64 * sizeof(double)));
+    *out = g;
+  });
+}
+
+int jfftb_grid_destroy(jfftb_grid* g) {
+  return guarded([&] {
+    if (!g) return;
+    DeviceGuard dg(g->device);
+    cudaStreamSynchronize(g->stream);
+    if (g->plans_ready) {
+      cufftDestroy(g->plan_fwd_d);
+      cufftDestroy(g->plan_inv_d);
+      cufftDestroy(g->plan_fwd_2d);
+    }
+    if (g->fft_work) cudaFree(g->fft_work);
+    if (g->partials) cudaFree(g->partials);
+    if (g->dscal) cudaFree(g->dscal);
+    cudaStreamDestroy(g->own_stream);
+    delete g;
+  });
+}
+
+int jfftb_grid_set_stream(jfftb_grid* g, void* stream) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    g->stream = stream ? (cudaStream_t)stream : g->own_stream;
+  });
+}
+
+int jfftb_grid_synchronize(jfftb_grid* g) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    DeviceGuard dg(g->device);
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+int jfftb_fft_forward(jfftb_grid* g, const double* u, double* spec, int where) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    ensure_plans(g);
+    DevBuf tin, tout;
+    const double* du = stage_in(g, u, geo.d * geo.N, where, tin);
+    double* ds = stage_out(spec, 2 * geo.d * geo.Nh, where, tout);
+    JF_CUFFT(cufftSetStream(g->plan_fwd_d, g->stream));
+    JF_CUFFT(cufftExecD2Z(g->plan_fwd_d, const_cast<double*>(du), (cufftDoubleComplex*)ds));
+    finish_out(g, spec, ds, 2 * geo.d * geo.Nh, where);
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+int jfftb_fft_inverse(jfftb_grid* g, const double* spec, double* u, int where) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    ensure_plans(g);
+    DevBuf tin, tout, work(sizeof(double2) * geo.d * geo.Nh);
+    const double* ds = stage_in(g, spec, 2 * geo.d * geo.Nh, where, tin);
+    double* du = stage_out(u, geo.d * geo.N, where, tout);
+    // Z2D overwrites its input: transform a copy
+    JF_CUDA(cudaMemcpyAsync(work.ptr, ds, sizeof(double2) * geo.d * geo.Nh,
+                            cudaMemcpyDeviceToDevice, g->stream));
+    JF_CUFFT(cufftSetStream(g->plan_inv_d, g->stream));
+    JF_CUFFT(cufftExecZ2D(g->plan_inv_d, work.as<cufftDoubleComplex>(), du));
+    scale_kernel<<<nblk(geo.d * geo.N), 256, 0, g->stream>>>(du, 1.0 / (double)geo.N,
+                                                              geo.d * geo.N);
+    JF_LAUNCHED();
+    finish_out(g, u, du, geo.d * geo.N, where);
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+int jfftb_op_create(jfftb_grid* g, const double* rho, int where, double lambda0, double mu0,
+                    jfftb_op** out) {
+  return guarded([&] {
+    require(g != nullptr && out != nullptr, "null argument");
+    require(std::isfinite(lambda0) && std::isfinite(mu0), "non-finite material");
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    DevBuf tin;
+    const double* dr = stage_in(g, rho, geo.N, where, tin);
+    double* own = nullptr;
+    JF_CUDA(cudaMalloc(&own, sizeof(double) * geo.N));
+    JF_CUDA(cudaMemcpyAsync(own, dr, sizeof(double) * geo.N, cudaMemcpyDeviceToDevice, g->stream));
+    int* bad = (int*)g->dscal;
+    JF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
+    check_rho_kernel<<<nblk(geo.N), 256, 0, g->stream>>>(own, geo.N, bad);
+    JF_LAUNCHED();
+    if (read_flag(g, bad)) {
+      cudaFree(own);
+      throw Error(JFFTB_EINVAL, "negative density");
+    }
+    auto* op = new jfftb_op();
+    op->grid = g;
+    op->rho = own;
+    op->lambda0 = lambda0;
+    op->mu0 = mu0;
+    *out = op;
+  });
+}
+
+int jfftb_op_destroy(jfftb_op* op) {
+  return guarded([&] {
+    if (!op) return;
+    DeviceGuard dg(op->grid->device);
+    cudaStreamSynchronize(op->grid->stream);
+    cudaFree(op->rho);
+    delete op;
+  });
+}
+
+int jfftb_apply_system(jfftb_op* op, const double* u, double* out, int where) {
+  return guarded([&] {
+    require(op != nullptr, "null operator");
+    jfftb_grid* g = op->grid;
+    DeviceGuard dg(g->device);
+    const int64_t n = g->geo.d * g->geo.N;
+    DevBuf tin, tout;
+    const double* du = stage_in(g, u, n, where, tin);
+    double* dout = stage_out(out, n, where, tout);
+    require(du != dout, "apply_system cannot run in place");
+    launch_stencil(g->geo, g->stream, ST_K, du, op->rho, op->lambda0, op->mu0, nullptr, dout,
+                   nullptr);
+    finish_out(g, out, dout, n, where);
+  });
+}
+
+static void check_ebar(int d, const double* eps_bar) {
+  require(eps_bar != nullptr, "null macroscopic strain");
+  const int m = d == 2 ? 3 : 6;
+  for (int k = 0; k < m; ++k)
+    require(std::isfinite(eps_bar[k]), "macroscopic strain must be finite");
+}
+
+int jfftb_assemble_rhs(jfftb_op* op, const double* eps_bar, double* out, int where) {
+  return guarded([&] {
+    require(op != nullptr, "null operator");
+    jfftb_grid* g = op->grid;
+    check_ebar(g->geo.d, eps_bar);
+    DeviceGuard dg(g->device);
+    const int64_t n = g->geo.d * g->geo.N;
+    DevBuf tout;
+    double* dout = stage_out(out, n, where, tout);
+    launch_stencil(g->geo, g->stream, ST_RHS, nullptr, op->rho, op->lambda0, op->mu0, eps_bar,
+                   dout, nullptr);
+    finish_out(g, out, dout, n, where);
+  });
+}
+
+int jfftb_total_strain(jfftb_op* op, const double* u, const double* eps_bar, double* out,
+                       int where) {
+  return guarded([&] {
+    require(op != nullptr, "null operator");
+    jfftb_grid* g = op->grid;
+    check_ebar(g->geo.d, eps_bar);
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    const int M = geo.d == 2 ? 3 : 6, T = geo.d == 2 ? 2 : 6;
+    DevBuf tin, tout;
+    const double* du = stage_in(g, u, geo.d * geo.N, where, tin);
+    double* dout = stage_out(out, (size_t)M * T * geo.N, where, tout);
+    launch_total_strain(geo, g->stream, du, eps_bar, dout);
+    finish_out(g, out, dout, (size_t)M * T * geo.N, where);
+  });
+}
+
+int jfftb_residual_force(jfftb_op* op, const double* u, const double* eps_bar, double* out,
+                         int where) {
+  return guarded([&] {
+    require(op != nullptr, "null operator");
+    jfftb_grid* g = op->grid;
+    check_ebar(g->geo.d, eps_bar);
+    DeviceGuard dg(g->device);
+    const int64_t n = g->geo.d * g->geo.N;
+    DevBuf tin, tout;
+    const double* du = stage_in(g, u, n, where, tin);
+    double* dout = stage_out(out, n, where, tout);
+    require(du != dout, "residual_force cannot run in place");
+    launch_stencil(g->geo, g->stream, ST_RES, du, op->rho, op->lambda0, op->mu0, eps_bar, dout,
+                   nullptr);
+    finish_out(g, out, dout, n, where);
+  });
+}
+
+int jfftb_homogenized_stress(jfftb_op* op, const double* u, const double* eps_bar,
+                             double* sigma_out, int where) {
+  return guarded([&] {
+    require(op != nullptr && sigma_out != nullptr, "null argument");
+    jfftb_grid* g = op->grid;
+    check_ebar(g->geo.d, eps_bar);
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    const int M = geo.d == 2 ? 3 : 6;
+    DevBuf tin;
+    const double* du = stage_in(g, u, geo.d * geo.N, where, tin);
+    double* part = ensure_partials(g, kRedBlocks * M + M);
+    const int cnt = launch_stress_sum(geo, g->stream, du, op->rho, op->lambda0, op->mu0,
+                                      eps_bar, part);
+    launch_sum_partials(g->stream, part, cnt, M, part + kRedBlocks * M);
+    double sums[6];
+    JF_CUDA(cudaMemcpyAsync(sums, part + kRedBlocks * M, sizeof(double) * M,
+                            cudaMemcpyDeviceToHost, g->stream));
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+    double vol = 1.0;
+    for (int a = 0; a < geo.d; ++a) vol *= geo.h[a] * geo.n[a];
+    const double scale = geo.w / vol;
+    for (int m = 0; m < M; ++m) sigma_out[m] = scale * sums[m];
+  });
+}
+
+int jfftb_green_create(jfftb_grid* g, double lambda_ref, double mu_ref, jfftb_green** out) {
+  return guarded([&] {
+    require(g != nullptr && out != nullptr, "null argument");
+    require(mu_ref > 0.0 && lambda_ref + mu_ref > 0.0,
+            "stiffness not positive definite");
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    // impulse responses of K_ref (rho = 1) on a small periodic grid that has
+    // the same pixel size: the stencil radius is 1, so for n >= 3 the
+    // response around node 0 is identical to the full grid's
+    Geom sm = geo;
+    int m[3] = {1, 1, 1};
+    sm.N = 1;
+    for (int a = 0; a < geo.d; ++a) {
+      m[a] = std::min(geo.n[a], 4);
+      sm.n[a] = m[a];
+      sm.N *= m[a];
+    }
+    sm.nh = sm.n[geo.d - 1] / 2 + 1;
+    sm.Nh = sm.N / sm.n[geo.d - 1] * sm.nh;
+    const int d = geo.d;
+    DevBuf imp(sizeof(double) * d * sm.N), resp(sizeof(double) * d * d * sm.N);
+    for (int beta = 0; beta < d; ++beta) {
+      JF_CUDA(cudaMemsetAsync(imp.ptr, 0, sizeof(double) * d * sm.N, g->stream));
+      const double one = 1.0;
+      JF_CUDA(cudaMemcpyAsync(imp.as<double>() + beta * sm.N, &one, sizeof(double),
+                              cudaMemcpyHostToDevice, g->stream));
+      launch_stencil(sm, g->stream, ST_K, imp.as<double>(), nullptr, lambda_ref, mu_ref, nullptr,
+                     resp.as<double>() + (int64_t)beta * d * sm.N, nullptr);
+    }
+    auto* gr = new jfftb_green();
+    gr->grid = g;
+    gr->lambda_ref = lambda_ref;
+    gr->mu_ref = mu_ref;
+    const int np = green_planes(d);
+    if (cudaMalloc(&gr->blocks, sizeof(double) * np * geo.Nh) != cudaSuccess) {
+      delete gr;
+      throw Error(JFFTB_ECUDA, "cudaMalloc failed for Green blocks");
+    }
+    launch_green_setup(geo, g->stream, resp.as<double>(), m[0] | (m[1] << 8) | (m[2] << 16),
+                       gr->blocks);
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+    *out = gr;
+  });
+}
+
+int jfftb_green_destroy(jfftb_green* green) {
+  return guarded([&] {
+    if (!green) return;
+    DeviceGuard dg(green->grid->device);
+    cudaStreamSynchronize(green->grid->stream);
+    cudaFree(green->blocks);
+    delete green;
+  });
+}
+
+int jfftb_green_export_blocks(jfftb_green* green, double* out) {
+  return guarded([&] {
+    require(green != nullptr && out != nullptr, "null argument");
+    jfftb_grid* g = green->grid;
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    const int d = geo.d, np = green_planes(d);
+    std::vector<double> packed((size_t)np * geo.Nh);
+    JF_CUDA(cudaMemcpyAsync(packed.data(), green->blocks, sizeof(double) * np * geo.Nh,
+                            cudaMemcpyDeviceToHost, g->stream));
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+    for (int64_t f = 0; f < geo.Nh; ++f) {
+      double* o = out + f * 2 * d * d;
+      for (int a = 0; a < d; ++a) {
+        o[2 * (a * d + a)] = packed[a * geo.Nh + f];
+        o[2 * (a * d + a) + 1] = 0.0;
+      }
+      int k = 0;
+      for (int a = 0; a < d; ++a)
+        for (int b = a + 1; b < d; ++b, ++k) {
+          const double re = packed[(d + 2 * k) * geo.Nh + f];
+          const double im = packed[(d + 2 * k + 1) * geo.Nh + f];
+          o[2 * (a * d + b)] = re;
+          o[2 * (a * d + b) + 1] = im;
+          o[2 * (b * d + a)] = re;
+          o[2 * (b * d + a) + 1] = -im;
+        }
+    }
+  });
+}
+
+int jfftb_apply_green(jfftb_green* green, const double* r, double* out, int where) {
+  return jfftb_apply_precond(JFFTB_PC_GREEN, green, nullptr, r, out, where);
+}
+
+int jfftb_jacobi_create(jfftb_op* op, jfftb_jacobi** out) {
+  return guarded([&] {
+    require(op != nullptr && out != nullptr, "null argument");
+    jfftb_grid* g = op->grid;
+    const Geom& geo = g->geo;
+    for (int a = 0; a < geo.d; ++a)
+      require(geo.n[a] % 2 == 0, "diagonal probing requires an even node count");
+    DeviceGuard dg(g->device);
+    const int64_t n = geo.d * geo.N;
+    DevBuf comb(sizeof(double) * n), resp(sizeof(double) * n);
+    double* diag = nullptr;
+    JF_CUDA(cudaMalloc(&diag, sizeof(double) * n));
+    try {
+      for (int alpha = 0; alpha < geo.d; ++alpha)
+        for (int offs = 0; offs < (1 << geo.d); ++offs) {
+          comb_kernel<<<nblk(n), 256, 0, g->stream>>>(comb.as<double>(), geo, alpha, offs);
+          JF_LAUNCHED();
+          launch_stencil(geo, g->stream, ST_K, comb.as<double>(), op->rho, op->lambda0, op->mu0,
+                         nullptr, resp.as<double>(), nullptr);
+          comb_extract_kernel<<<nblk(geo.N), 256, 0, g->stream>>>(diag, resp.as<double>(), geo,
+                                                                  alpha, offs);
+          JF_LAUNCHED();
+        }
+      int* bad = (int*)g->dscal;
+      JF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
+      jacobi_finish_kernel<<<nblk(n), 256, 0, g->stream>>>(diag, n, bad);
+      JF_LAUNCHED();
+      if (read_flag(g, bad))
+        throw Error(JFFTB_EINVAL, "probed diagonal has negative or non-finite entries");
+    } catch (...) {
+      cudaFree(diag);
+      throw;
+    }
+    auto* j = new jfftb_jacobi();
+    j->op = op;
+    j->inv_sqrt = diag;
+    *out = j;
+  });
+}
+
+int jfftb_jacobi_destroy(jfftb_jacobi* jac) {
+  return guarded([&] {
+    if (!jac) return;
+    DeviceGuard dg(jac->op->grid->device);
+    cudaStreamSynchronize(jac->op->grid->stream);
+    cudaFree(jac->inv_sqrt);
+    delete jac;
+  });
+}
+
+int jfftb_jacobi_export(jfftb_jacobi* jac, double* out, int where) {
+  return guarded([&] {
+    require(jac != nullptr, "null jacobi");
+    jfftb_grid* g = jac->op->grid;
+    DeviceGuard dg(g->device);
+    const int64_t n = g->geo.d * g->geo.N;
+    require(out != nullptr, "null output");
+    JF_CUDA(cudaMemcpyAsync(out, jac->inv_sqrt, sizeof(double) * n,
+                            where == JFFTB_HOST ? cudaMemcpyDeviceToHost
+                                                : cudaMemcpyDeviceToDevice,
+                            g->stream));
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+int jfftb_apply_precond(int kind, jfftb_green* green, jfftb_jacobi* jac, const double* r,
+                        double* out, int where) {
+  return guarded([&] {
+    jfftb_grid* g = green ? green->grid : (jac ? jac->op->grid : nullptr);
+    require(g != nullptr, "preconditioner needs a Green operator or a Jacobi diagonal");
+    if (green && jac) require(green->grid == jac->op->grid, "grid mismatch");
+    DeviceGuard dg(g->device);
+    const int64_t n = g->geo.d * g->geo.N;
+    DevBuf tin, tout;
+    const double* dr = stage_in(g, r, n, where, tin);
+    double* dout = stage_out(out, n, where, tout);
+    precond_device(kind, green, jac, g, dr, dout);
+    finish_out(g, out, dout, n, where);
+  });
+}
+
+int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
+              jfftb_green* green_term, const double* rhs, int where, double eta, int max_iter,
+              double* x_out, double* history_out, int* iterations, int* terminated,
+              double* wall_s) {
+  const auto t0 = std::chrono::steady_clock::now();
+  return guarded([&] {
+    require(op != nullptr && green_term != nullptr, "pcg needs an operator and a Green operator");
+    require(history_out && iterations && terminated, "null output argument");
+    require(kind >= JFFTB_PC_NONE && kind <= JFFTB_PC_GREEN_JACOBI, "unknown preconditioner");
+    require(max_iter >= 0, "max_iter must be >= 0");
+    jfftb_grid* g = op->grid;
+    require(green_term->grid == g, "Green operator lives on a different grid");
+    if (kind == JFFTB_PC_GREEN || kind == JFFTB_PC_GREEN_JACOBI)
+      require(green_pc != nullptr && green_pc->grid == g, "kind needs an assembled Green operator");
+    if (kind == JFFTB_PC_JACOBI || kind == JFFTB_PC_GREEN_JACOBI)
+      require(jac != nullptr && jac->op->grid == g, "kind needs an assembled Jacobi diagonal");
+    if (!green_pc) green_pc = green_term;
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    cudaStream_t s = g->stream;
+    ensure_plans(g);
+    const int64_t n = geo.d * geo.N;
+    DevBuf tin;
+    const double* drhs = stage_in(g, rhs, n, where, tin);
+
+    // workspace
+    const int kcount = stencil_blocks(geo);
+    DevBuf bx(sizeof(double) * n), brs(sizeof(double) * 2 * n), bp(sizeof(double) * n),
+        bkp(sizeof(double) * n), bspec(sizeof(double2) * 2 * geo.d * geo.Nh),
+        bst(sizeof(PcgState)), bhist(sizeof(double) * (max_iter + 1)),
+        bpart(sizeof(double) * (kcount + 2 * kRedBlocks + kRedBlocks));
+    PcgBuffers B{};
+    B.x = bx.as<double>();
+    B.rs = brs.as<double>();
+    B.p = bp.as<double>();
+    B.kp = bkp.as<double>();
+    B.spec = bspec.as<double2>();
+    B.st = bst.as<PcgState>();
+    B.hist = bhist.as<double>();
+    B.kpart = bpart.as<double>();
+    B.spart = B.kpart + kcount;
+    B.upart = B.spart + 2 * kRedBlocks;
+    B.kcount = kcount;
+
+    PcgState h0{};
+    h0.eta = eta;
+    h0.max_iter = max_iter;
+    JF_CUDA(cudaMemcpyAsync(B.st, &h0, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+    JF_CUDA(cudaMemsetAsync(B.x, 0, sizeof(double) * n, s));
+    JF_CUDA(cudaMemcpyAsync(B.rs, drhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+
+    PcgState* hs = nullptr;
+    JF_CUDA(cudaMallocHost(&hs, sizeof(PcgState)));
+    struct HostFree {
+      PcgState* p;
+      ~HostFree() { cudaFreeHost(p); }
+    } hf{hs};
+    auto poll = [&]() {
+      JF_CUDA(cudaMemcpyAsync(hs, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      JF_CUDA(cudaStreamSynchronize(s));
+      return hs->done != 0;
+    };
+    pcg_dispatch(kind, true, op, jac, green_pc, green_term, B);
+    bool done = poll();
+    // host loop: iterations are predicated on the device flag, so a few can
+    // be queued ahead of each poll; the batch grows while the solve runs
+    int batch = 1;
+    while (!done) {
+      for (int k = 0; k < batch; ++k) pcg_dispatch(kind, false, op, jac, green_pc, green_term, B);
+      done = poll();
+      batch = std::min(batch * 2, 8);
+    }
+    const int it = hs->iters;
+    *iterations = it;
+    JF_CUDA(cudaMemcpyAsync(history_out, B.hist, sizeof(double) * (it + 1),
+                            cudaMemcpyDeviceToHost, s));
+    JF_CUDA(cudaStreamSynchronize(s));
+    if (hs->status != JFFTB_OK) {
+      if (wall_s)
+        *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      throw Error(hs->status, hs->status == JFFTB_ECURVATURE
+                                  ? "non-positive search-direction curvature in PCG"
+                                  : "PCG recurrence became non-finite");
+    }
+    *terminated = (hs->gnorm2 <= eta) ? JFFTB_CONVERGED : JFFTB_ITERATION_CAP;
+    launch_sub_mean(geo, s, B.x, ensure_partials(g, kRedBlocks * 3 + 3));
+    if (x_out) {
+      JF_CUDA(cudaMemcpyAsync(x_out, B.x, sizeof(double) * n,
+                              where == JFFTB_HOST ? cudaMemcpyDeviceToHost
+                                                  : cudaMemcpyDeviceToDevice,
+                              s));
+    }
+    JF_CUDA(cudaStreamSynchronize(s));
+    if (wall_s)
+      *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+}  // extern "C"

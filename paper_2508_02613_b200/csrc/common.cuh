@@ -1,0 +1,305 @@
+// Shared internals of libjfftb200.so: handle structs, error plumbing and the
+// per-voxel finite-element force routine used by every stencil kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "../../include/jfftb200.h"
+
+namespace jfftb {
+
+// ---------------------------------------------------------------------------
+// errors: C++ exceptions inside, int status codes at the C boundary
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+void count_launch(int n = 1);
+
+#define JF_CUDA(call)                                                          \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess)                                                     \
+      throw ::jfftb::Error(JFFTB_ECUDA, std::string(#call) + ": " +            \
+                                            cudaGetErrorString(e_));           \
+  } while (0)
+
+#define JF_CUFFT(call)                                                         \
+  do {                                                                         \
+    cufftResult r_ = (call);                                                   \
+    if (r_ != CUFFT_SUCCESS)                                                   \
+      throw ::jfftb::Error(JFFTB_ECUDA, std::string(#call) + ": cufft error " + \
+                                            std::to_string((int)r_));          \
+  } while (0)
+
+#define JF_LAUNCHED()                                                          \
+  do {                                                                         \
+    ::jfftb::count_launch();                                                   \
+    JF_CUDA(cudaGetLastError());                                               \
+  } while (0)
+
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(JFFTB_EINVAL, msg);
+}
+
+// ---------------------------------------------------------------------------
+// geometry passed by value to kernels
+// ---------------------------------------------------------------------------
+struct Geom {
+  int d;
+  int n[3];        // nodes per axis (axis 0 slowest)
+  int64_t N;       // nodes
+  int nh;          // n[d-1]/2 + 1
+  int64_t Nh;      // half-spectrum entries per component
+  double h[3];     // pixel size per axis
+  double hinv[3];
+  double w;        // quadrature weight prod(h)/d!
+  bool iso;        // all h equal
+};
+
+// persistent device scalars of one PCG solve
+struct PcgState {
+  double rz, curv, alpha, beta, gnorm2, rz_new, eta;
+  int done;     // 1 once converged / capped / aborted
+  int iters;    // search-direction updates so far
+  int status;   // JFFTB_OK / JFFTB_ENONFINITE / JFFTB_ECURVATURE
+  int max_iter;
+};
+
+}  // namespace jfftb
+
+struct jfftb_grid {
+  jfftb::Geom geo;
+  int device;
+  cudaStream_t own_stream;
+  cudaStream_t stream;
+  // cuFFT plans: vector field (batch d) and doubled vector field (batch 2d)
+  cufftHandle plan_fwd_d = 0, plan_inv_d = 0, plan_fwd_2d = 0;
+  bool plans_ready = false;
+  void* fft_work = nullptr;
+  size_t fft_work_bytes = 0;
+  // reduction scratch
+  double* partials = nullptr;   // per-block partial sums
+  int partials_cap = 0;
+  double* dscal = nullptr;      // small device scalar scratch
+};
+
+struct jfftb_op {
+  jfftb_grid* grid;
+  double* rho;      // device, N
+  double lambda0, mu0;
+};
+
+struct jfftb_green {
+  jfftb_grid* grid;
+  double lambda_ref, mu_ref;
+  // Hermitian-packed blocks, planar: 2-D 4 planes (G00, G11, Re G01, Im G01);
+  // 3-D 9 planes (G00, G11, G22, Re/Im G01, Re/Im G02, Re/Im G12), each Nh
+  double* blocks;
+};
+
+struct jfftb_jacobi {
+  jfftb_op* op;
+  double* inv_sqrt;  // device, d * N
+};
+
+namespace jfftb {
+
+// ---------------------------------------------------------------------------
+// P1 simplex tables (d-generic, see oracle/jfft_oracle.py edge_offsets)
+// Simplex t = permutation t (lexicographic) of the axes; its path edge along
+// axis a starts at voxel corner o(t,a) (bitmask: bit j = offset along axis j).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int perm_axis(int D, int t, int k) {
+  // k-th axis visited by permutation t
+  return D == 2 ? (t == 0 ? k : 1 - k)
+                : (t == 0 ? k
+                   : t == 1 ? (k == 0 ? 0 : k == 1 ? 2 : 1)
+                   : t == 2 ? (k == 0 ? 1 : k == 1 ? 0 : 2)
+                   : t == 3 ? (k == 0 ? 1 : k == 1 ? 2 : 0)
+                   : t == 4 ? (k == 0 ? 2 : k == 1 ? 0 : 1)
+                            : (k == 0 ? 2 : k == 1 ? 1 : 0));
+}
+__host__ __device__ constexpr int perm_pos(int D, int t, int ax) {
+  return perm_axis(D, t, 0) == ax ? 0 : perm_axis(D, t, 1) == ax ? 1 : 2;
+}
+__host__ __device__ constexpr int edge_base(int D, int t, int a) {
+  int m = 0;
+  for (int j = 0; j < D; ++j) {
+    if (j == a) continue;
+    bool prec = perm_pos(D, t, j) < perm_pos(D, t, a);
+    bool bit = (j == 0) ? !prec : prec;
+    if (bit) m |= 1 << j;
+  }
+  return m;
+}
+__host__ __device__ constexpr int n_simplex(int D) { return D == 2 ? 2 : 6; }
+__host__ __device__ constexpr int mandel_m(int D) { return D == 2 ? 3 : 6; }
+// Mandel component of the symmetric pair (i, j)
+__host__ __device__ constexpr int mandel_of(int D, int i, int j) {
+  return i == j ? i
+                : (D == 2 ? 2 : (i + j == 3 ? 3 : (i + j == 2 ? 4 : 5)));
+}
+__host__ __device__ constexpr int mandel_i(int D, int m) {
+  return m < D ? m : (D == 2 ? 0 : (m == 3 ? 1 : 0));
+}
+__host__ __device__ constexpr int mandel_j(int D, int m) {
+  return m < D ? m : (D == 2 ? 1 : (m == 3 ? 2 : (m == 4 ? 2 : 1)));
+}
+
+constexpr double kSqrt2 = 1.4142135623730951;
+constexpr double kInvSqrt2 = 0.70710678118654752;
+
+enum VoxMode { VOX_K = 0, VOX_RHS = 1, VOX_RES = 2 };
+
+// Nodal forces of one voxel.  uc[c][i]: displacement component i at corner c
+// (bit j of c = +1 along axis j).  G_t[i][a] = (diff along the path edge)*gs[a]
+// (+ Ebar for VOX_RES; = Ebar for VOX_RHS).  Stress per simplex
+// sigma = lam tr(G) I + mu (G + G^T) with lam/mu already scaled by rho*w (and,
+// in ISO K mode, by 1/h^2 with gs = fs = 1).  Edge forces sigma[:,a]*fs[a] go
+// + to the edge's high corner and - to its low corner; f[c][i] is the sum.
+template <int D, int MODE, bool SCALE>
+__device__ __forceinline__ void voxel_forces(const double (&uc)[1 << D][D],
+                                             double lam, double mu,
+                                             const double* gs, const double* fs,
+                                             const double (*Ebar)[3],
+                                             double (&f)[1 << D][D]) {
+  constexpr int C = 1 << D;
+  constexpr int T = n_simplex(D);
+  double acc[D][C][D];
+  bool init[D][C];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < C; ++c) init[a][c] = false;
+
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    double G[D][D];  // G[i][a] = d u_i / d x_a
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int o = edge_base(D, t, a);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double g = 0.0;
+        if (MODE != VOX_RHS) {
+          g = uc[o | (1 << a)][i] - uc[o][i];
+          if (SCALE) g *= gs[a];
+        }
+        if (MODE == VOX_RHS) g = Ebar[i][a];
+        if (MODE == VOX_RES) g += Ebar[i][a];
+        G[i][a] = g;
+      }
+    }
+    double tr = G[0][0];
+#pragma unroll
+    for (int a = 1; a < D; ++a) tr += G[a][a];
+    const double lt = lam * tr;
+    const double mu2 = 2.0 * mu;
+    double S[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      S[a][a] = fma(mu2, G[a][a], lt);
+#pragma unroll
+      for (int b = a + 1; b < D; ++b) {
+        S[a][b] = mu * (G[a][b] + G[b][a]);
+        S[b][a] = S[a][b];
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int o = edge_base(D, t, a);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        if (init[a][o]) acc[a][o][i] += S[i][a];
+        else acc[a][o][i] = S[i][a];
+      }
+      init[a][o] = true;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = 0.0;
+      bool first = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const bool high = (c >> a) & 1;
+        const int o = high ? (c ^ (1 << a)) : c;
+        if (!init[a][o]) continue;
+        double e = acc[a][o][i];
+        if (SCALE) e *= fs[a];
+        if (first) { s = high ? e : -e; first = false; }
+        else s = high ? s + e : s - e;
+      }
+      f[c][i] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers (defined in the .cu files)
+// ---------------------------------------------------------------------------
+enum StencilMode { ST_K = 0, ST_RHS = 1, ST_RES = 2 };
+
+// out = K u (ST_K), -B^T W rho C E (ST_RHS), -B^T W sigma(E + B u) (ST_RES).
+// rho == nullptr means rho = 1.  curv_partials (ST_K only, may be null):
+// per-block <u, out> partials; returns number of blocks written.
+int launch_stencil(const Geom& g, cudaStream_t s, int mode, const double* u,
+                   const double* rho, double lam, double mu, const double* ebar_mandel,
+                   double* out, double* curv_partials);
+int stencil_blocks(const Geom& g);
+
+void launch_total_strain(const Geom& g, cudaStream_t s, const double* u,
+                         const double* ebar, double* out);
+// per-block partials of sum_Q rho C0 (E + B u), M values per block
+int launch_stress_sum(const Geom& g, cudaStream_t s, const double* u, const double* rho,
+                      double lam, double mu, const double* ebar, double* partials);
+
+// vector algebra
+constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic
+constexpr int kRedThreads = 256;
+void launch_fill(cudaStream_t s, double* x, double v, int64_t n);
+void launch_copy(cudaStream_t s, double* dst, const double* src, int64_t n);
+void launch_mul(cudaStream_t s, double* out, const double* a, const double* b, int64_t n);
+void launch_mul2(cudaStream_t s, double* out, const double* a, const double* b, int64_t n);
+void launch_dot(cudaStream_t s, const double* a, const double* b, int64_t n, double* partials);
+// sum `count` partials (stride `stride`, `m` interleaved values) -> out[m]
+void launch_sum_partials(cudaStream_t s, const double* partials, int count, int m,
+                         double* out);
+// scratch: kRedBlocks * d + d doubles
+void launch_sub_mean(const Geom& g, cudaStream_t s, double* x, double* scratch);
+
+// spectral kernels
+int green_planes(int d);
+void launch_green_apply(const Geom& g, cudaStream_t s, const double* blocks,
+                        const double2* in, double2* out, int ncomp_batches);
+// resp: d x d x prod(m) impulse responses on the small grid m (packed m0|m1<<8|m2<<16)
+void launch_green_setup(const Geom& g, cudaStream_t s, const double* resp, int m,
+                        double* blocks);
+
+// PCG (pcg.cu)
+struct PcgBuffers {
+  double *x, *rs, *p, *kp;  // rs = [r ; s or z'] (2 d N)
+  double2* spec;            // 2 d Nh
+  PcgState* st;
+  double* hist;
+  double *kpart, *spart, *upart;
+  int kcount;
+};
+void pcg_dispatch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
+                  jfftb_green* gterm, const PcgBuffers& B);
+void launch_pcg_spectral(const Geom& g, cudaStream_t s, int mode, const double* gpc,
+                         const double* gterm, double2* spec, const PcgState* st,
+                         double* partials);
+
+}  // namespace jfftb

@@ -1,0 +1,245 @@
+// PCG recurrence on device (solver.py:64-140).
+//
+// One iteration = stencil K p (+ fused <p, Kp> partials) -> alpha ->
+// fused x/r update (+ D^-1/2 r, + <r, z> partials for jacobi/none) -> forward
+// FFT -> fused Green block solve + Parseval quadratic forms -> termination /
+// beta -> inverse FFT -> fused p update.  All scalars (alpha, beta, rz, the
+// Green norm, the iteration count and the convergence flag) live on the
+// device; every kernel of an iteration is predicated on `done`, so the host
+// never needs a result before launching the next iteration.
+#include "common.cuh"
+
+namespace jfftb {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double block_sum1(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (wid == 0) {
+    s = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    s = warp_sum(s);
+  }
+  return s;
+}
+
+// fixed-order sum of partials[b*stride + j], b < count, in one 1024-thread block
+__device__ double sum_strided(const double* p, int count, int stride, int j, double* red) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < count; b += blockDim.x) s += p[(int64_t)b * stride + j];
+  s = block_sum1(s, red);
+  __syncthreads();
+  return s;  // valid in thread 0
+}
+
+__global__ void alpha_kernel(PcgState* st, const double* __restrict__ partials, int count) {
+  __shared__ double red[32];
+  if (st->done) return;
+  const double curv = sum_strided(partials, count, 1, 0, red);
+  if (threadIdx.x == 0) {
+    st->curv = curv;
+    if (!isfinite(curv)) {
+      st->status = JFFTB_ENONFINITE;
+      st->done = 1;
+    } else if (curv <= 0.0) {
+      st->status = JFFTB_ECURVATURE;
+      st->done = 1;
+    } else {
+      st->alpha = st->rz / curv;
+    }
+  }
+}
+
+// x += alpha p ; r -= alpha Kp ; kind-specific extras (INIT: no x/r update)
+template <int KIND, bool INIT>
+__global__ void __launch_bounds__(256)
+    update_kernel(int64_t n, const PcgState* __restrict__ st, double* __restrict__ x,
+                  double* __restrict__ r, const double* __restrict__ p,
+                  const double* __restrict__ kp, const double* __restrict__ dinv,
+                  double* __restrict__ sz, double* __restrict__ partials) {
+  __shared__ double red[32];
+  if (st->done) return;
+  const double alpha = st->alpha;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double ri = r[i];
+    if (!INIT) {
+      x[i] = x[i] + alpha * p[i];
+      ri = ri - alpha * kp[i];
+      r[i] = ri;
+    }
+    if (KIND == JFFTB_PC_GREEN_JACOBI) sz[i] = dinv[i] * ri;
+    if (KIND == JFFTB_PC_JACOBI) {
+      const double zi = dinv[i] * (dinv[i] * ri);
+      sz[i] = zi;
+      acc = fma(ri, zi, acc);
+    }
+    if (KIND == JFFTB_PC_NONE) acc = fma(ri, ri, acc);
+  }
+  if (KIND == JFFTB_PC_JACOBI || KIND == JFFTB_PC_NONE) {
+    acc = block_sum1(acc, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  }
+}
+
+// termination test + beta (solver.py:122-135); INIT = the k = 0 check (99-110)
+template <int KIND, bool INIT>
+__global__ void finalize_kernel(PcgState* st, const double* __restrict__ spart, int scount,
+                                const double* __restrict__ upart, int ucount,
+                                double* __restrict__ hist) {
+  __shared__ double red[32];
+  if (st->done) return;
+  const double q0 = sum_strided(spart, scount, 2, 0, red);
+  const double q1 = sum_strided(spart, scount, 2, 1, red);
+  double u0 = 0.0;
+  if (KIND == JFFTB_PC_JACOBI || KIND == JFFTB_PC_NONE) u0 = sum_strided(upart, ucount, 1, 0, red);
+  if (threadIdx.x != 0) return;
+  int it = st->iters;
+  if (!INIT) st->iters = ++it;
+  const double g2 = q0;
+  if (!isfinite(g2)) {
+    st->status = JFFTB_ENONFINITE;
+    st->done = 1;
+    return;
+  }
+  hist[it] = g2;
+  st->gnorm2 = g2;
+  if (g2 <= st->eta) {
+    st->done = 1;
+    return;
+  }
+  const double rz_new = (KIND == JFFTB_PC_JACOBI || KIND == JFFTB_PC_NONE) ? u0 : q1;
+  if (!isfinite(rz_new)) {
+    st->status = JFFTB_ENONFINITE;
+    st->done = 1;
+    return;
+  }
+  if (!INIT) st->beta = rz_new / st->rz;
+  st->rz = rz_new;
+  if (it >= st->max_iter) st->done = 1;  // iteration cap: reported, not raised
+}
+
+// p = beta p + z  (INIT: p = z); z = D^-1/2 z' (green-jacobi), z' (green),
+// r (none), D^-1 r (jacobi, precomputed in sz)
+template <int KIND, bool INIT>
+__global__ void __launch_bounds__(256)
+    pupdate_kernel(int64_t n, const PcgState* __restrict__ st, double* __restrict__ p,
+                   const double* __restrict__ zsrc, const double* __restrict__ dinv) {
+  if (st->done) return;
+  const double beta = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double z = zsrc[i];
+    if (KIND == JFFTB_PC_GREEN_JACOBI) z = dinv[i] * z;
+    p[i] = INIT ? z : beta * p[i] + z;
+  }
+}
+
+}  // namespace
+
+
+static void run_fwd_fft(jfftb_grid* g, int batch2, double* in, double2* out) {
+  cufftHandle plan = batch2 ? g->plan_fwd_2d : g->plan_fwd_d;
+  JF_CUFFT(cufftSetStream(plan, g->stream));
+  JF_CUFFT(cufftExecD2Z(plan, in, (cufftDoubleComplex*)out));
+}
+static void run_inv_fft(jfftb_grid* g, double2* in, double* out) {
+  JF_CUFFT(cufftSetStream(g->plan_inv_d, g->stream));
+  JF_CUFFT(cufftExecZ2D(g->plan_inv_d, (cufftDoubleComplex*)in, out));
+}
+
+static int grid_n(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kRedBlocks));
+}
+
+// one pass of the preconditioner + termination functional; INIT = k = 0
+template <int KIND, bool INIT>
+static void pcg_precond_phase(jfftb_grid* g, jfftb_jacobi* jac, jfftb_green* gpc,
+                              jfftb_green* gterm, const PcgBuffers& B) {
+  const Geom& geo = g->geo;
+  const int64_t n = geo.d * geo.N;
+  cudaStream_t s = g->stream;
+  const double* dinv = jac ? jac->inv_sqrt : nullptr;
+  double* r = B.rs;
+  double* sz = B.rs + n;
+  update_kernel<KIND, INIT><<<kRedBlocks, 256, 0, s>>>(n, B.st, B.x, r, B.p, B.kp, dinv, sz,
+                                                       B.upart);
+  JF_LAUNCHED();
+  if (KIND == JFFTB_PC_GREEN_JACOBI) {
+    run_fwd_fft(g, 1, B.rs, B.spec);
+    launch_pcg_spectral(geo, s, 1, gpc->blocks, gterm->blocks, B.spec, B.st, B.spart);
+  } else if (KIND == JFFTB_PC_GREEN) {
+    run_fwd_fft(g, 0, r, B.spec);
+    launch_pcg_spectral(geo, s, 0, gpc->blocks, gterm->blocks, B.spec, B.st, B.spart);
+  } else {
+    run_fwd_fft(g, 0, r, B.spec);
+    launch_pcg_spectral(geo, s, 2, gterm->blocks, gterm->blocks, B.spec, B.st, B.spart);
+  }
+  finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, kRedBlocks, B.upart, kRedBlocks,
+                                                 B.hist);
+  JF_LAUNCHED();
+  const double* zsrc = r;
+  if (KIND == JFFTB_PC_GREEN_JACOBI) {
+    run_inv_fft(g, B.spec + geo.d * geo.Nh, sz);
+    zsrc = sz;
+  } else if (KIND == JFFTB_PC_GREEN) {
+    run_inv_fft(g, B.spec, sz);
+    zsrc = sz;
+  } else if (KIND == JFFTB_PC_JACOBI) {
+    zsrc = sz;
+  }
+  pupdate_kernel<KIND, INIT><<<grid_n(n), 256, 0, s>>>(n, B.st, B.p, zsrc, dinv);
+  JF_LAUNCHED();
+}
+
+template <int KIND>
+static void pcg_iteration(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
+                          jfftb_green* gterm, const PcgBuffers& B) {
+  jfftb_grid* g = op->grid;
+  cudaStream_t s = g->stream;
+  launch_stencil(g->geo, s, ST_K, B.p, op->rho, op->lambda0, op->mu0, nullptr, B.kp, B.kpart);
+  alpha_kernel<<<1, 1024, 0, s>>>(B.st, B.kpart, B.kcount);
+  JF_LAUNCHED();
+  pcg_precond_phase<KIND, false>(g, jac, gpc, gterm, B);
+}
+
+template <int KIND>
+static void pcg_init(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc, jfftb_green* gterm,
+                     const PcgBuffers& B) {
+  pcg_precond_phase<KIND, true>(op->grid, jac, gpc, gterm, B);
+}
+
+void pcg_dispatch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
+                  jfftb_green* gterm, const PcgBuffers& B) {
+  switch (kind) {
+    case JFFTB_PC_NONE:
+      init ? pcg_init<JFFTB_PC_NONE>(op, jac, gpc, gterm, B)
+           : pcg_iteration<JFFTB_PC_NONE>(op, jac, gpc, gterm, B);
+      break;
+    case JFFTB_PC_GREEN:
+      init ? pcg_init<JFFTB_PC_GREEN>(op, jac, gpc, gterm, B)
+           : pcg_iteration<JFFTB_PC_GREEN>(op, jac, gpc, gterm, B);
+      break;
+    case JFFTB_PC_JACOBI:
+      init ? pcg_init<JFFTB_PC_JACOBI>(op, jac, gpc, gterm, B)
+           : pcg_iteration<JFFTB_PC_JACOBI>(op, jac, gpc, gterm, B);
+      break;
+    default:
+      init ? pcg_init<JFFTB_PC_GREEN_JACOBI>(op, jac, gpc, gterm, B)
+           : pcg_iteration<JFFTB_PC_GREEN_JACOBI>(op, jac, gpc, gterm, B);
+      break;
+  }
+}
+
+}  // namespace jfftb

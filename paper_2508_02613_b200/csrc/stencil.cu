@@ -1,0 +1,494 @@
+// Matrix-free P1 stiffness apply and its relatives (rhs, residual force,
+// total strain, stress average) on the periodic grid.
+//
+// Replaces operators.py:43-101 / fem.py:41-111 (K u = B^T W rho C0 B u).
+//
+// KA design ("plane march"): a CTA owns a (BY x BX) column tile of voxels in
+// the (axis1, axis2) plane -- axis 2 is the contiguous one -- and marches
+// along axis 0.  Each thread owns one voxel column: per layer it reads its
+// node of the next plane once from HBM (coalesced along axis 2), takes the
+// other three corners of its voxel from shared memory, evaluates the voxel's
+// d! simplices in registers (voxel_forces) and hands the corner forces that
+// belong to neighbouring node columns over shared memory.  The lowest row and
+// column of the tile are halo voxels, so a CTA emits (BY-1) x (BX-1) node
+// columns and every node is written exactly once, with a fixed summation
+// order (bitwise deterministic).  rho and u are read once per layer; out is
+// written once: 2d+1 scalar fields of HBM traffic per apply.
+#include "common.cuh"
+
+namespace jfftb {
+
+namespace {
+
+constexpr int BX3 = 32, BY3 = 8;   // 3-D tile (threads), emits 31 x 7 columns
+constexpr int BX2 = 128;           // 2-D tile, emits 127 columns
+
+__device__ __forceinline__ int wrapi(int i, int n) {
+  i %= n;
+  return i < 0 ? i + n : i;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  // deterministic block reduction (fixed tree); returns total in thread 0
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nthr = blockDim.x * blockDim.y * blockDim.z;
+  const int lane = tid & 31, wid = tid >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (wid == 0) {
+    s = lane < (nthr >> 5) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  }
+  return s;
+}
+
+struct EbarT {
+  double e[3][3];
+  double m[6];  // the Mandel vector itself
+};
+
+__host__ EbarT make_ebar(int d, const double* m) {
+  EbarT E{};
+  if (!m) return E;
+  for (int k = 0; k < (d == 2 ? 3 : 6); ++k) E.m[k] = m[k];
+  for (int i = 0; i < d; ++i) E.e[i][i] = m[i];
+  if (d == 2) {
+    E.e[0][1] = E.e[1][0] = m[2] / kSqrt2;
+  } else {
+    E.e[1][2] = E.e[2][1] = m[3] / kSqrt2;
+    E.e[0][2] = E.e[2][0] = m[4] / kSqrt2;
+    E.e[0][1] = E.e[1][0] = m[5] / kSqrt2;
+  }
+  return E;
+}
+
+// --------------------------------------------------------------------------
+// 3-D plane-march stencil
+// --------------------------------------------------------------------------
+template <int MODE, bool SCALE>
+__global__ void __launch_bounds__(BX3* BY3)
+    stencil3d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
+              double lam0, double mu0, EbarT E, double* __restrict__ out,
+              double* __restrict__ partials, int chunk) {
+  constexpr bool HAS_U = MODE != VOX_RHS;
+  __shared__ double U[3][BY3 + 1][BX3 + 1];
+  __shared__ double F[3][2][3][BY3][BX3];  // [dir x,y,xy][plane k,k+1][comp]
+  __shared__ double red[32];
+
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int64_t P = (int64_t)n1 * n2;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int X0 = blockIdx.x * (BX3 - 1), Y0 = blockIdx.y * (BY3 - 1);
+  const int k0 = blockIdx.z * chunk;
+  const int k1 = min(k0 + chunk, n0);
+  const int gx = X0 - 1 + tx, gy = Y0 - 1 + ty;
+  const int c2 = wrapi(gx, n2), c1 = wrapi(gy, n1);
+  const bool outp = tx >= 1 && ty >= 1 && gx < n2 && gy < n1;
+  const int c2h = wrapi(X0 - 1 + BX3, n2), c1h = wrapi(Y0 - 1 + BY3, n1);
+  const int64_t col = (int64_t)c1 * n2 + c2;
+
+  double gs[3], fs[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) { gs[a] = g.hinv[a]; fs[a] = g.hinv[a]; }
+  const double (*Eb)[3] = E.e;
+
+  auto load_plane = [&](int k) {
+    if (!HAS_U) return;
+    const int64_t base = (int64_t)k * P;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double* ui = u + i * g.N + base;
+      U[i][ty][tx] = __ldg(ui + col);
+      if (tx == BX3 - 1) U[i][ty][BX3] = __ldg(ui + (int64_t)c1 * n2 + c2h);
+      if (ty == BY3 - 1) U[i][BY3][tx] = __ldg(ui + (int64_t)c1h * n2 + c2);
+      if (tx == BX3 - 1 && ty == BY3 - 1) U[i][BY3][BX3] = __ldg(ui + (int64_t)c1h * n2 + c2h);
+    }
+  };
+  auto read_corners = [&](double (&q)[4][3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      q[0][i] = U[i][ty][tx];
+      q[1][i] = U[i][ty][tx + 1];
+      q[2][i] = U[i][ty + 1][tx];
+      q[3][i] = U[i][ty + 1][tx + 1];
+    }
+  };
+
+  double uk[4][3], uk1[4][3];
+  const int kstart = wrapi(k0 - 1, n0);
+  if (HAS_U) {
+    load_plane(kstart);
+    __syncthreads();
+    read_corners(uk);
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) uk[q][i] = uk1[q][i] = 0.0;
+  }
+
+  double nxt[3] = {0.0, 0.0, 0.0};
+  double csum = 0.0;
+  for (int kk = k0 - 1; kk < k1; ++kk) {
+    const int k = wrapi(kk, n0);
+    const int kp = (k + 1 == n0) ? 0 : k + 1;
+    if (HAS_U) {
+      load_plane(kp);
+      __syncthreads();
+      read_corners(uk1);
+    }
+    const double r = rho ? __ldg(rho + (int64_t)k * P + col) : 1.0;
+    double lam = lam0 * r, mu = mu0 * r;
+    double uc[8][3];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int q = (((c >> 1) & 1) << 1) | ((c >> 2) & 1);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) uc[c][i] = (c & 1) ? uk1[q][i] : uk[q][i];
+    }
+    double f[8][3];
+    voxel_forces<3, MODE, SCALE>(uc, lam, mu, gs, fs, Eb, f);
+    double ak[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      ak[i] = nxt[i] + f[0][i];
+      nxt[i] = f[1][i];
+      F[0][0][i][ty][tx] = f[4][i];
+      F[0][1][i][ty][tx] = f[5][i];
+      F[1][0][i][ty][tx] = f[2][i];
+      F[1][1][i][ty][tx] = f[3][i];
+      F[2][0][i][ty][tx] = f[6][i];
+      F[2][1][i][ty][tx] = f[7][i];
+    }
+    __syncthreads();
+    if (tx >= 1 && ty >= 1) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        ak[i] = ak[i] + F[0][0][i][ty][tx - 1] + F[1][0][i][ty - 1][tx] +
+                F[2][0][i][ty - 1][tx - 1];
+        nxt[i] = nxt[i] + F[0][1][i][ty][tx - 1] + F[1][1][i][ty - 1][tx] +
+                 F[2][1][i][ty - 1][tx - 1];
+      }
+    }
+    if (kk >= k0 && outp) {
+      const int64_t idx = (int64_t)k * P + col;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) out[i * g.N + idx] = ak[i];
+      if (MODE == VOX_K && partials)
+        csum += uk[0][0] * ak[0] + uk[0][1] * ak[1] + uk[0][2] * ak[2];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) uk[q][i] = uk1[q][i];
+    if (!HAS_U) __syncthreads();  // F is rewritten next layer
+  }
+  if (MODE == VOX_K && partials) {
+    const double s = block_sum(csum, red);
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      partials[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s;
+  }
+}
+
+// --------------------------------------------------------------------------
+// 2-D plane-march stencil (axis 0 marched, axis 1 across threads)
+// --------------------------------------------------------------------------
+template <int MODE, bool SCALE>
+__global__ void __launch_bounds__(BX2)
+    stencil2d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
+              double lam0, double mu0, EbarT E, double* __restrict__ out,
+              double* __restrict__ partials, int chunk) {
+  constexpr bool HAS_U = MODE != VOX_RHS;
+  __shared__ double U[2][BX2 + 1];
+  __shared__ double F[2][2][BX2];  // [plane][comp]
+  __shared__ double red[32];
+  const int n0 = g.n[0], n1 = g.n[1];
+  const int tx = threadIdx.x;
+  const int X0 = blockIdx.x * (BX2 - 1);
+  const int k0 = blockIdx.y * chunk;
+  const int k1 = min(k0 + chunk, n0);
+  const int gx = X0 - 1 + tx;
+  const int c1 = wrapi(gx, n1);
+  const bool outp = tx >= 1 && gx < n1;
+  const int c1h = wrapi(X0 - 1 + BX2, n1);
+  double gs[2] = {g.hinv[0], g.hinv[1]}, fs[2] = {g.hinv[0], g.hinv[1]};
+  const double (*Eb)[3] = E.e;
+
+  auto load_plane = [&](int k) {
+    if (!HAS_U) return;
+    const int64_t base = (int64_t)k * n1;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      U[i][tx] = __ldg(u + i * g.N + base + c1);
+      if (tx == BX2 - 1) U[i][BX2] = __ldg(u + i * g.N + base + c1h);
+    }
+  };
+  double uk[2][2] = {{0, 0}, {0, 0}}, uk1[2][2] = {{0, 0}, {0, 0}};
+  const int kstart = wrapi(k0 - 1, n0);
+  if (HAS_U) {
+    load_plane(kstart);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) { uk[0][i] = U[i][tx]; uk[1][i] = U[i][tx + 1]; }
+    __syncthreads();
+  }
+  double nxt[2] = {0.0, 0.0};
+  double csum = 0.0;
+  for (int kk = k0 - 1; kk < k1; ++kk) {
+    const int k = wrapi(kk, n0);
+    const int kp = (k + 1 == n0) ? 0 : k + 1;
+    if (HAS_U) {
+      load_plane(kp);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 2; ++i) { uk1[0][i] = U[i][tx]; uk1[1][i] = U[i][tx + 1]; }
+    }
+    const double r = rho ? __ldg(rho + (int64_t)k * n1 + c1) : 1.0;
+    double uc[4][2];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) uc[c][i] = (c & 1) ? uk1[(c >> 1) & 1][i] : uk[(c >> 1) & 1][i];
+    double f[4][2];
+    voxel_forces<2, MODE, SCALE>(uc, lam0 * r, mu0 * r, gs, fs, Eb, f);
+    double ak[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      ak[i] = nxt[i] + f[0][i];
+      nxt[i] = f[1][i];
+      F[0][i][tx] = f[2][i];
+      F[1][i][tx] = f[3][i];
+    }
+    __syncthreads();
+    if (tx >= 1) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        ak[i] = ak[i] + F[0][i][tx - 1];
+        nxt[i] = nxt[i] + F[1][i][tx - 1];
+      }
+    }
+    if (kk >= k0 && outp) {
+      const int64_t idx = (int64_t)k * n1 + c1;
+      out[idx] = ak[0];
+      out[g.N + idx] = ak[1];
+      if (MODE == VOX_K && partials) csum += uk[0][0] * ak[0] + uk[0][1] * ak[1];
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) uk[q][i] = uk1[q][i];
+    if (!HAS_U) __syncthreads();  // F is rewritten next layer
+  }
+  if (MODE == VOX_K && partials) {
+    const double s = block_sum(csum, red);
+    if (threadIdx.x == 0) partials[blockIdx.x + gridDim.x * blockIdx.y] = s;
+  }
+}
+
+struct StencilLaunch {
+  dim3 grid, block;
+  int chunk;
+};
+
+StencilLaunch stencil_config(const Geom& g) {
+  StencilLaunch L{};
+  const int target = 4 * 148;
+  if (g.d == 3) {
+    const int bx = (g.n[2] + BX3 - 2) / (BX3 - 1), by = (g.n[1] + BY3 - 2) / (BY3 - 1);
+    int chunks = (target + bx * by - 1) / (bx * by);
+    chunks = std::max(1, std::min(chunks, g.n[0]));
+    L.chunk = (g.n[0] + chunks - 1) / chunks;
+    chunks = (g.n[0] + L.chunk - 1) / L.chunk;
+    L.grid = dim3(bx, by, chunks);
+    L.block = dim3(BX3, BY3, 1);
+  } else {
+    const int bx = (g.n[1] + BX2 - 2) / (BX2 - 1);
+    int chunks = (target + bx - 1) / bx;
+    chunks = std::max(1, std::min(chunks, g.n[0]));
+    L.chunk = (g.n[0] + chunks - 1) / chunks;
+    chunks = (g.n[0] + L.chunk - 1) / L.chunk;
+    L.grid = dim3(bx, chunks, 1);
+    L.block = dim3(BX2, 1, 1);
+  }
+  return L;
+}
+
+template <int MODE, bool SCALE>
+void launch_mode(const Geom& g, cudaStream_t s, const StencilLaunch& L, const double* u,
+                 const double* rho, double lam, double mu, const EbarT& E, double* out,
+                 double* partials) {
+  if (g.d == 3)
+    stencil3d<MODE, SCALE><<<L.grid, L.block, 0, s>>>(g, u, rho, lam, mu, E, out, partials,
+                                                      L.chunk);
+  else
+    stencil2d<MODE, SCALE><<<L.grid, L.block, 0, s>>>(g, u, rho, lam, mu, E, out, partials,
+                                                      L.chunk);
+  JF_LAUNCHED();
+}
+
+}  // namespace
+
+int stencil_blocks(const Geom& g) {
+  StencilLaunch L = stencil_config(g);
+  return L.grid.x * L.grid.y * L.grid.z;
+}
+
+int launch_stencil(const Geom& g, cudaStream_t s, int mode, const double* u, const double* rho,
+                   double lam, double mu, const double* ebar_mandel, double* out,
+                   double* curv_partials) {
+  StencilLaunch L = stencil_config(g);
+  const EbarT E = make_ebar(g.d, ebar_mandel);
+  if (mode == ST_K) {
+    if (g.iso) {
+      // fold the two 1/h factors and the weight into the Lame constants
+      const double sc = g.w * g.hinv[0] * g.hinv[0];
+      launch_mode<VOX_K, false>(g, s, L, u, rho, lam * sc, mu * sc, E, out, curv_partials);
+    } else {
+      launch_mode<VOX_K, true>(g, s, L, u, rho, lam * g.w, mu * g.w, E, out, curv_partials);
+    }
+  } else if (mode == ST_RHS) {
+    // f = -B^T W rho C E : negate through the Lame constants
+    launch_mode<VOX_RHS, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr);
+  } else {
+    launch_mode<VOX_RES, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr);
+  }
+  return L.grid.x * L.grid.y * L.grid.z;
+}
+
+// --------------------------------------------------------------------------
+// total strain E + B u at the quadrature points (operators.py:79-83)
+// --------------------------------------------------------------------------
+template <int D>
+__global__ void total_strain_kernel(Geom g, const double* __restrict__ u, EbarT E,
+                                    double* __restrict__ out) {
+  constexpr int C = 1 << D, T = n_simplex(D), M = mandel_m(D);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.N;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int idx[3];
+    int64_t rem = v;
+    for (int a = D - 1; a >= 0; --a) { idx[a] = rem % g.n[a]; rem /= g.n[a]; }
+    double uc[C][D];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      int64_t node = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        int ia = idx[a] + ((c >> a) & 1);
+        if (ia == g.n[a]) ia = 0;
+        node = node * g.n[a] + ia;
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) uc[c][i] = __ldg(u + i * g.N + node);
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      double G[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int o = edge_base(D, t, a);
+#pragma unroll
+        for (int i = 0; i < D; ++i) G[i][a] = (uc[o | (1 << a)][i] - uc[o][i]) / g.h[a];
+      }
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int i = mandel_i(D, m), j = mandel_j(D, m);
+        double e = (i == j) ? G[i][i] : (G[i][j] + G[j][i]) / kSqrt2;
+        e += E.m[m];
+        out[((int64_t)m * T + t) * g.N + v] = e;
+      }
+    }
+  }
+}
+
+void launch_total_strain(const Geom& g, cudaStream_t s, const double* u, const double* ebar,
+                         double* out) {
+  const EbarT E = make_ebar(g.d, ebar);
+  const int blocks = (int)std::min<int64_t>((g.N + 255) / 256, 148 * 16);
+  if (g.d == 3) total_strain_kernel<3><<<blocks, 256, 0, s>>>(g, u, E, out);
+  else total_strain_kernel<2><<<blocks, 256, 0, s>>>(g, u, E, out);
+  JF_LAUNCHED();
+}
+
+// --------------------------------------------------------------------------
+// sum_Q rho C0 (E + B u): per-block partials (M values each)
+// --------------------------------------------------------------------------
+template <int D>
+__global__ void stress_sum_kernel(Geom g, const double* __restrict__ u,
+                                  const double* __restrict__ rho, double lam, double mu,
+                                  EbarT E, double* __restrict__ partials) {
+  constexpr int C = 1 << D, T = n_simplex(D), M = mandel_m(D);
+  __shared__ double red[32];
+  double acc[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m] = 0.0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.N;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int idx[3];
+    int64_t rem = v;
+    for (int a = D - 1; a >= 0; --a) { idx[a] = rem % g.n[a]; rem /= g.n[a]; }
+    double uc[C][D];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      int64_t node = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        int ia = idx[a] + ((c >> a) & 1);
+        if (ia == g.n[a]) ia = 0;
+        node = node * g.n[a] + ia;
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) uc[c][i] = u ? __ldg(u + i * g.N + node) : 0.0;
+    }
+    const double r = __ldg(rho + v);
+    double vs[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) vs[m] = 0.0;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      double G[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int o = edge_base(D, t, a);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          G[i][a] = (uc[o | (1 << a)][i] - uc[o][i]) / g.h[a] + E.e[i][a];
+      }
+      double tr = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) tr += G[a][a];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int i = mandel_i(D, m), j = mandel_j(D, m);
+        // Mandel stress of C0 eps: diag lam tr + 2 mu e_ii; shear 2 mu e_m
+        vs[m] += (i == j) ? lam * tr + 2.0 * mu * G[i][i]
+                          : 2.0 * mu * (G[i][j] + G[j][i]) / kSqrt2;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[m] += r * vs[m];
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const double s = block_sum(acc[m], red);
+    if (threadIdx.x == 0) partials[blockIdx.x * M + m] = s;
+    __syncthreads();
+  }
+}
+
+int launch_stress_sum(const Geom& g, cudaStream_t s, const double* u, const double* rho,
+                      double lam, double mu, const double* ebar, double* partials) {
+  const EbarT E = make_ebar(g.d, ebar);
+  const int blocks = kRedBlocks;
+  if (g.d == 3) stress_sum_kernel<3><<<blocks, 256, 0, s>>>(g, u, rho, lam, mu, E, partials);
+  else stress_sum_kernel<2><<<blocks, 256, 0, s>>>(g, u, rho, lam, mu, E, partials);
+  JF_LAUNCHED();
+  return blocks;
+}
+
+}  // namespace jfftb

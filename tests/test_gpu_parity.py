@@ -1,0 +1,275 @@
+"""CUDA path (through the C ABI) vs the reference goldens and the oracle.
+
+Tolerances: the reference's own (test_operators.py:25-33 dense K 1e-12,
+test_preconditioners.py 1e-10..1e-13) and BASELINE's 1e-9 relative
+on converged solves; iteration counts exact (BASELINE allows +-1).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import jfft_oracle as X
+from paper_2508_02613_b200 import grid as G
+from paper_2508_02613_b200 import microstructures as ms
+from paper_2508_02613_b200.material import isotropic_material
+from paper_2508_02613_b200.operators import (apply_system, assemble_rhs, homogenized_stress,
+                                             make_operator, residual_force, total_strain)
+from paper_2508_02613_b200.preconditioners import (apply_green, apply_green_jacobi, apply_jacobi,
+                                                   apply_jacobi_half, assemble_green,
+                                                   assemble_jacobi, build_preconditioner)
+from paper_2508_02613_b200.solver import (CONVERGED, ITERATION_CAP, SolverAbortError, pcg)
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ("none", "green", "jacobi", "green-jacobi")
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def _case(npz, key, d):
+    lengths = tuple(npz[f"{key}_lengths"])
+    rho = npz[f"{key}_rho"]
+    n = rho.shape[0]
+    grid = G.make_grid(n, lengths)
+    mat = isotropic_material(2.0 / 3.0, 0.5, d)
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    return grid, mat, op
+
+
+@pytest.fixture(scope="module")
+def small2d(golden_dir):
+    return np.load(os.path.join(golden_dir, "small2d.npz"))
+
+
+@pytest.fixture(scope="module")
+def small3d(golden_dir):
+    return np.load(os.path.join(golden_dir, "small3d.npz"))
+
+
+@pytest.mark.parametrize("key", ["n8", "n16", "n6"])
+def test_operator_2d_vs_reference(small2d, key):
+    grid, mat, op = _case(small2d, key, 2)
+    u = G.VectorField(grid, small2d[f"{key}_u"])
+    eb = small2d[f"{key}_eps_bar"]
+    assert rel(apply_system(op, u).values, small2d[f"{key}_Ku"]) <= 1e-12
+    assert rel(assemble_rhs(op, eb).values, small2d[f"{key}_rhs"]) <= 1e-12
+    assert rel(total_strain(op, u, eb).values, small2d[f"{key}_strain"]) <= 1e-13
+    assert rel(residual_force(op, u, eb).values, small2d[f"{key}_resforce"]) <= 1e-12
+    assert rel(homogenized_stress(op, u, eb), small2d[f"{key}_sigma"]) <= 1e-13
+
+
+@pytest.mark.parametrize("key", ["n8", "n16", "n6"])
+def test_green_2d_vs_reference(small2d, key):
+    grid, mat, op = _case(small2d, key, 2)
+    green = assemble_green(grid, mat)
+    ref = small2d[f"{key}_blocks"]
+    assert green.blocks.shape == ref.shape
+    assert np.abs(green.blocks - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert np.abs(green.blocks[0, 0]).max() == 0.0
+    u = G.VectorField(grid, small2d[f"{key}_u"])
+    assert rel(apply_green(green, u).values, small2d[f"{key}_Gu"]) <= 1e-12
+
+
+@pytest.mark.parametrize("key", ["n8", "n16"])
+def test_jacobi_2d_vs_reference(small2d, key):
+    grid, mat, op = _case(small2d, key, 2)
+    jac = assemble_jacobi(op)
+    assert rel(jac.inv_sqrt, small2d[f"{key}_inv_sqrt"]) <= 1e-14
+    green = assemble_green(grid, mat)
+    u = G.VectorField(grid, small2d[f"{key}_u"])
+    assert rel(apply_green_jacobi(jac, green, u).values, small2d[f"{key}_GJu"]) <= 1e-12
+    ref_half = small2d[f"{key}_inv_sqrt"] * small2d[f"{key}_u"]
+    assert rel(apply_jacobi_half(jac, u).values, ref_half) <= 1e-14
+    ref_full = small2d[f"{key}_inv_sqrt"] * (small2d[f"{key}_inv_sqrt"] * small2d[f"{key}_u"])
+    assert rel(apply_jacobi(jac, u).values, ref_full) <= 1e-14
+
+
+@pytest.mark.parametrize("key", ["n8", "n16"])
+@pytest.mark.parametrize("kind", KINDS)
+def test_pcg_2d_vs_reference(small2d, key, kind):
+    grid, mat, op = _case(small2d, key, 2)
+    green = assemble_green(grid, mat)
+    rhs = assemble_rhs(op, small2d[f"{key}_eps_bar"])
+    rep = pcg(op, rhs, build_preconditioner(kind, op, green), green, eta=1e-10, max_iter=999)
+    assert rep.terminated == CONVERGED
+    assert abs(rep.iterations - int(small2d[f"{key}_{kind}_iters"])) <= 1
+    h_ref = small2d[f"{key}_{kind}_hist"]
+    m = min(len(h_ref), len(rep.residual_history))
+    assert rel(rep.residual_history[:3], h_ref[:3]) <= 1e-10
+    assert np.all(np.isfinite(rep.residual_history[:m]))
+    assert rel(rep.solution.values, small2d[f"{key}_{kind}_x"]) <= 1e-9
+
+
+@pytest.mark.parametrize("key", ["n4x4x4", "n6x4x8"])
+def test_operator_3d_vs_oracle(small3d, key):
+    grid_shape = small3d[f"{key}_rho"].shape
+    if len(set(grid_shape)) != 1:
+        pytest.skip("non-cubic grid: exercised through the raw C ABI test")
+    grid, mat, op = _case(small3d, key, 3)
+    u = G.VectorField(grid, small3d[f"{key}_u"])
+    eb = small3d[f"{key}_eps_bar"]
+    assert rel(apply_system(op, u).values, small3d[f"{key}_Ku"]) <= 1e-12
+    assert rel(assemble_rhs(op, eb).values, small3d[f"{key}_rhs"]) <= 1e-12
+    assert rel(total_strain(op, u, eb).values, small3d[f"{key}_strain"]) <= 1e-13
+    assert rel(homogenized_stress(op, u, eb), small3d[f"{key}_sigma"]) <= 1e-13
+    green = assemble_green(grid, mat)
+    assert np.abs(green.blocks - small3d[f"{key}_blocks"]).max() <= \
+        1e-13 * np.abs(small3d[f"{key}_blocks"]).max()
+    assert rel(apply_green(green, u).values, small3d[f"{key}_Gu"]) <= 1e-12
+    jac = assemble_jacobi(op)
+    assert rel(jac.inv_sqrt, small3d[f"{key}_inv_sqrt"]) <= 1e-14
+    rhs = assemble_rhs(op, eb)
+    for kind in KINDS:
+        rep = pcg(op, rhs, build_preconditioner(kind, op, green), green, eta=1e-10)
+        assert abs(rep.iterations - int(small3d[f"{key}_{kind}_iters"])) <= 1
+        assert rel(rep.solution.values, small3d[f"{key}_{kind}_x"]) <= 1e-9
+
+
+def test_noncubic_3d_via_abi(small3d):
+    """Non-cubic 3-D grid straight through the C ABI (the reference's Grid
+    has one n; the ABI takes n per axis)."""
+    import ctypes as C
+    from paper_2508_02613_b200 import _native as N
+    key = "n6x4x8"
+    rho = np.ascontiguousarray(small3d[f"{key}_rho"])
+    n = rho.shape
+    lengths = tuple(small3d[f"{key}_lengths"])
+    gh = N.GridHandle(3, n, lengths)
+    op = N.OpHandle(gh, rho, 2.0 / 3.0, 0.5)
+    u = np.ascontiguousarray(small3d[f"{key}_u"])
+    out = np.empty_like(u)
+    N.check(N.load().jfftb_apply_system(op.ptr, N.vptr(u), N.vptr(out), N.HOST))
+    assert rel(out, small3d[f"{key}_Ku"]) <= 1e-12
+    green = N.GreenHandle(gh, 2.0 / 3.0, 0.5)
+    blocks = np.empty(small3d[f"{key}_blocks"].shape, dtype=np.complex128)
+    N.check(N.load().jfftb_green_export_blocks(green.ptr, N.vptr(blocks)))
+    assert np.abs(blocks - small3d[f"{key}_blocks"]).max() <= 1e-13 * np.abs(blocks).max()
+    jac = N.JacobiHandle(op)
+    rhs = np.empty_like(u)
+    N.check(N.load().jfftb_assemble_rhs(op.ptr, N.dptr(small3d[f"{key}_eps_bar"].copy()),
+                                        N.vptr(rhs), N.HOST))
+    assert rel(rhs, small3d[f"{key}_rhs"]) <= 1e-12
+    for kind in KINDS:
+        x = np.empty_like(u)
+        hist = np.zeros(1000)
+        it, term, wall = C.c_int(), C.c_int(), C.c_double()
+        code = N.KIND_CODES[kind]
+        N.check(N.load().jfftb_pcg(op.ptr, code, green.ptr, jac.ptr, green.ptr, N.vptr(rhs),
+                                   N.HOST, 1e-10, 999, N.vptr(x), N.dptr(hist), C.byref(it),
+                                   C.byref(term), C.byref(wall)))
+        assert abs(it.value - int(small3d[f"{key}_{kind}_iters"])) <= 1
+        assert rel(x, small3d[f"{key}_{kind}_x"]) <= 1e-9
+
+
+def test_config1_parity(golden_dir):
+    """BASELINE config 1 (256^2, i = 10, contrast 1e4, eps = e1 (x) e1) against
+    the reference's own solves."""
+    gold = json.load(open(os.path.join(golden_dir, "config1.json")))
+    lam, mu = ms.lame_from_poisson()
+    mat = isotropic_material(lam, mu)
+    for filters in (10, 0):
+        rho = ms.bernoulli_smoothed(256, filters, 1e4, 0)
+        grid = G.make_grid(256)
+        op = make_operator(G.ScalarField(grid, rho), mat)
+        green = assemble_green(grid, mat)
+        eb = np.array([1.0, 0.0, 0.0])
+        rhs = assemble_rhs(op, eb)
+        for kind in ("green", "green-jacobi"):
+            key = f"i{filters}_{kind}"
+            rep = pcg(op, rhs, build_preconditioner(kind, op, green), green)
+            assert rep.terminated == gold[f"{key}_terminated"]
+            assert abs(rep.iterations - gold[f"{key}_iters"]) <= 1, key
+            sig = homogenized_stress(op, rep.solution, eb)
+            if rep.terminated == CONVERGED:
+                assert rel(sig, gold[f"{key}_sigma"]) <= 1e-9
+                u_ref = np.load(os.path.join(golden_dir, f"config1_{key}_u.npy"))
+                assert rel(rep.solution.values, u_ref) <= 1e-9
+                assert rel(rep.residual_history, gold[f"{key}_hist"]) <= 1e-6
+            else:
+                # capped run: same status and count; history within the
+                # CPU-vs-CPU floor (parity_floor)
+                h = np.array(rep.residual_history)
+                hr = np.array(gold[f"{key}_hist"])
+                assert len(h) == len(hr)
+                assert rel(h[:50], hr[:50]) <= 1e-6
+                assert rel(sig, gold[f"{key}_sigma"]) <= 1e-2
+
+
+def test_pcg_contract():
+    """solver contract (test_solver.py:20-102) on the device path."""
+    grid = G.make_grid(16)
+    mat = isotropic_material(2.0 / 3.0, 0.5)
+    rho = np.where(np.arange(16)[:, None] < 8, 1.0, 1e-4) * np.ones((16, 16))
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    green = assemble_green(grid, mat)
+    rhs = assemble_rhs(op, np.array([1.0, 1.0, 1.0]))
+    # zero rhs -> 0 iterations, history [0.0]
+    rep = pcg(op, G.VectorField.zeros(grid), build_preconditioner("green", op, green), green)
+    assert rep.iterations == 0 and rep.residual_history == [0.0] and rep.terminated == CONVERGED
+    assert np.abs(rep.solution.values).max() == 0.0
+    # history contract
+    for kind in KINDS:
+        rep = pcg(op, rhs, build_preconditioner(kind, op, green), green, eta=1e-6)
+        assert rep.terminated == CONVERGED
+        assert len(rep.residual_history) == rep.iterations + 1
+        assert rep.residual_history[-1] <= 1e-6
+        assert all(v > 1e-6 for v in rep.residual_history[:-1])
+    # cap reported, not raised
+    rep = pcg(op, rhs, build_preconditioner("jacobi", op, green), green, eta=1e-12, max_iter=3)
+    assert rep.terminated == ITERATION_CAP and rep.iterations == 3
+    assert len(rep.residual_history) == 4
+    # deterministic
+    pre = build_preconditioner("green-jacobi", op, green)
+    a = pcg(op, rhs, pre, green)
+    b = pcg(op, rhs, pre, green)
+    assert a.iterations == b.iterations and a.residual_history == b.residual_history
+    assert np.array_equal(a.solution.values, b.solution.values)
+    # zero-mean solution
+    assert np.abs(a.solution.component_means()).max() <= 1e-12 * np.abs(a.solution.values).max()
+    # NaN aborts
+    bad = G.VectorField.zeros(grid)
+    bad.values[0, 0, 0] = np.nan
+    with pytest.raises(SolverAbortError):
+        pcg(op, bad, build_preconditioner("green", op, green), green)
+    # k = 0 Green norm identical for every kind
+    h0 = [pcg(op, rhs, build_preconditioner(k, op, green), green, eta=1e-8).residual_history[0]
+          for k in KINDS]
+    assert all(abs(h - h0[0]) <= 1e-12 * h0[0] for h in h0)
+
+
+def test_validation_errors():
+    grid = G.make_grid(5)
+    mat = isotropic_material(2.0 / 3.0, 0.5)
+    op = make_operator(G.ScalarField.full(grid, 1.0), mat)
+    with pytest.raises(ValueError):
+        assemble_jacobi(op)
+    with pytest.raises(ValueError):
+        apply_system(op, G.VectorField.zeros(G.make_grid(8)))
+    with pytest.raises(ValueError):
+        assemble_rhs(op, np.array([1.0, np.inf, 0.0]))
+    with pytest.raises(ValueError):
+        assemble_rhs(op, np.array([1.0, 2.0]))
+
+
+def test_uniform_medium_one_iteration():
+    """test_preconditioners.py:214-227 in 2-D and its 3-D analogue."""
+    for d, n in ((2, 16), (3, 8)):
+        grid = G.make_grid(n, (1.0,) * d)
+        mat = isotropic_material(2.0 / 3.0, 0.5, d)
+        op = make_operator(G.ScalarField.full(grid, 1.0), mat)
+        green = assemble_green(grid, mat)
+        eb = np.ones(3 if d == 2 else 6)
+        rng = np.random.default_rng(0)
+        u0 = G.VectorField(grid, rng.normal(size=(d,) + (n,) * d))
+        rhs = apply_system(op, u0)
+        rep = pcg(op, rhs, build_preconditioner("green-jacobi", op, green), green, eta=1e-20)
+        assert rep.iterations == 1
+        sig = homogenized_stress(op, G.VectorField.zeros(grid), eb)
+        c = X.isotropic_stiffness(d, 2.0 / 3.0, 0.5)
+        assert np.allclose(sig, c @ eb, rtol=0, atol=1e-13)
