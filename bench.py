@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""J-FFT PCG throughput on B200 (BASELINE.json metric: GDOF-iterations/s, fp64,
+3-D 512^3, and the fraction of the HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload 3d512|3d128|2d2048] [--kind green-jacobi|green]
+
+A "step" is one fixed-length PCG solve (``--iters`` iterations, eta = -1 so
+no early exit) over the resident synthetic problem: BASELINE config 4, a
+512^3 crack-disc damage field (E = (1-phi)^2 + 1e-4, nu = 0.3, eps_xx = 1),
+Green-Jacobi preconditioner.  value = d * N * iterations * K / time / 1e9.
+Only the PCG iterations are credited; each step's init (k = 0 preconditioner
+application) and the final mean subtraction run inside the timed region.
+
+--impl reference times the reference algorithm's CPU implementation (the
+NumPy oracle port, oracle/jfft_oracle.py -- the reference is pure Python and
+cannot be built into oracle/_ref) on the host's cores with the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOADS = {
+    # name: (d, n, generator, eps_bar)
+    "3d512": (3, 512, "cracks", [1.0, 0, 0, 0, 0, 0]),
+    "3d128": (3, 128, "spheres", [1.0, 0, 0, 0, 0, 0]),
+    "2d2048": (2, 2048, "bernoulli20", [0.0, 0.0, np.sqrt(2.0) * 0.5]),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="3d512", choices=sorted(WORKLOADS))
+    ap.add_argument("--kind", default="green-jacobi", choices=["green-jacobi", "green"])
+    ap.add_argument("--iters", type=int, default=20, help="PCG iterations per step")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peak_hbm():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle port on the host cores
+# ---------------------------------------------------------------------------
+_W = {}
+
+
+def _ref_worker_init(d, n, kind, seed):
+    from oracle import jfft_oracle as X
+    from paper_2508_02613_b200 import microstructures as ms
+    lam, mu = ms.lame_from_poisson()
+    if d == 3:
+        rho = ms.crack_discs(n, count=max(1, 64 * n ** 3 // 512 ** 3), seed=seed)
+        eb = np.array([1.0, 0, 0, 0, 0, 0])
+    else:
+        rho = ms.bernoulli_smoothed(n, 20, 1e4, seed)
+        eb = np.array([0.0, 0.0, np.sqrt(2.0) * 0.5])
+    c = X.isotropic_stiffness(d, lam, mu)
+    h = X.pixel_size((n,) * d, (1.0,) * d)
+    _W.update(X=X, rho=rho, c=c, h=h, kind=kind,
+              blocks=X.assemble_green((n,) * d, (1.0,) * d, c),
+              inv=X.assemble_jacobi(rho, c, h), rhs=X.assemble_rhs(rho, c, h, eb))
+
+
+def _ref_worker_solve(iters):
+    X = _W["X"]
+    t0 = time.perf_counter()
+    X.pcg(_W["rho"], _W["c"], _W["h"], _W["rhs"], _W["kind"], _W["blocks"], _W["inv"],
+          eta=-1.0, max_iter=iters)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_n(d):
+    return 64 if d == 3 else 256
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    import multiprocessing as mp
+    d, nfull, _, _ = WORKLOADS[args.workload]
+    n = cpu_sample_n(d)
+    cores = os.cpu_count() or 1
+    iters = 5
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_ref_worker_init, initargs=(d, n, args.kind, 0)) as pool:
+        for _ in range(max(args.warmup, 0)):
+            pool.map(_ref_worker_solve, [1] * cores)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_ref_worker_solve, [iters] * cores)
+        dt = time.perf_counter() - t0
+    dof_it = d * n ** d * iters * cores * args.steps
+    value = dof_it / dt / 1e9
+    sample = (f"{cores} concurrent oracle PCG solves ({args.kind}) of {n}^{d} per step, "
+              f"{iters} iterations each (full {nfull}^{d} does not fit a NumPy oracle)")
+    line = {
+        "impl": "reference", "metric": metric_name(args), "value": value, "unit": "GDOF-it/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args),
+        "cpu_baseline": {"value": value, "unit": "GDOF-it/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GDOF-it/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def cpu_baseline_single(args):
+    """The oracle port, 1 core, a bounded sample of the workload (rank 0, N=1)."""
+    d = WORKLOADS[args.workload][0]
+    n = cpu_sample_n(d)
+    _ref_worker_init(d, n, args.kind, 0)
+    _ref_worker_solve(1)
+    iters = 4
+    t = _ref_worker_solve(iters)
+    return {"value": d * n ** d * iters / t / 1e9, "unit": "GDOF-it/s", "cores": 1,
+            "kind": "port",
+            "sample": f"oracle PCG ({args.kind}) on a {n}^{d} sample of the workload "
+                      f"generator, {iters} iterations, {t:.1f} s, numpy single-threaded"}
+
+
+def metric_name(args):
+    d, n, _, _ = WORKLOADS[args.workload]
+    return f"J-FFT PCG GDOF-iterations/s (fp64, {d}D {n}^{d})"
+
+
+def config_of(args):
+    d, n, gen, _ = WORKLOADS[args.workload]
+    return {"workload": f"{args.workload}-{gen}-{args.kind}", "d": d, "n": n,
+            "kind": args.kind, "iterations_per_step": args.iters,
+            "mode": "fixed-iteration throughput (eta=-1); parity solves are in tests/",
+            "l2": "inputs larger than L2 (one vector field = %.1f GiB)" % (d * n ** d * 8 / 2 ** 30),
+            "parallelism": "replicas" if args.gpus > 1 else "single"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def build_problem(args, torch, dev):
+    from paper_2508_02613_b200 import _native as N
+    from paper_2508_02613_b200 import microstructures as ms
+    d, n, gen, eb = WORKLOADS[args.workload]
+    lam, mu = ms.lame_from_poisson()
+    shape = (n,) * d
+    if gen == "cracks":
+        rho = ms.crack_discs_device(n, seed=0, device=dev)
+    elif gen == "spheres":
+        rho = torch.from_numpy(ms.random_spheres(n, seed=0)).to(dev)
+    else:
+        rho = torch.from_numpy(ms.bernoulli_smoothed(n, 20, 1e4, 0)).to(dev)
+    gh = N.GridHandle(d, shape, (1.0,) * d, device=torch.cuda.current_device())
+    gh.set_stream(torch.cuda.current_stream().cuda_stream)
+    op = N.OpHandle(gh, rho.data_ptr(), lam, mu, where=N.DEVICE)
+    green = N.GreenHandle(gh, lam, mu)
+    jac = N.JacobiHandle(op) if args.kind == "green-jacobi" else None
+    rhs = torch.empty((d,) + shape, dtype=torch.float64, device=dev)
+    ebv = np.ascontiguousarray(eb, dtype=np.float64)
+    N.check(N.load().jfftb_assemble_rhs(op.ptr, N.dptr(ebv), rhs.data_ptr(), N.DEVICE))
+    x = torch.empty_like(rhs)
+    torch.cuda.synchronize()
+    return dict(d=d, n=n, N=n ** d, gh=gh, op=op, green=green, jac=jac, rhs=rhs, x=x, rho=rho,
+                lam=lam, mu=mu, eb=ebv)
+
+
+def run_ours(args, rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_02613_b200 import _native as N
+    from paper_2508_02613_b200 import roofline as R
+    from paper_2508_02613_b200.solver import pcg_device
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    P = build_problem(args, torch, dev)
+    d, Nn = P["d"], P["N"]
+
+    def step():
+        pcg_device(P["op"], args.kind, P["green"], P["jac"], P["rhs"].data_ptr(),
+                   P["x"].data_ptr(), -1.0, args.iters)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
+    N.launch_count(reset=True)
+    P["gh"].profile_start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = N.launch_count(reset=True)
+    stage_ms, prof_iters = P["gh"].profile_read(stop=True)
+    ms_total = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    iters_total = args.iters * args.steps
+    value = world * d * Nn * iters_total / (ms_total / 1e3) / 1e9
+
+    # ---- roofline: whole iteration (north star) and dominant stage --------
+    peak, peak_src = peak_hbm()
+    per_iter_ms = ms_total / iters_total
+    alg_iter = R.algorithmic_bytes(args.kind, d, Nn)
+    stages = {}
+    for k, nm in enumerate(R.STAGES):
+        if prof_iters:
+            avg = stage_ms[k] / prof_iters
+            b = R.kernel_bytes(nm, args.kind, d, Nn)
+            stages[nm] = {"ms": avg, "share": stage_ms[k] / max(stage_ms.sum(), 1e-30),
+                          "alg_bytes": b, "GBps": (b / (avg / 1e3) / 1e9) if avg > 0 and b else None}
+    ours = {k: v for k, v in stages.items() if not k.startswith("fft")}
+    dom_all = max(stages, key=lambda k: stages[k]["ms"]) if stages else None
+    dom = max(ours, key=lambda k: ours[k]["ms"]) if ours else None
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if dom and os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.workload}:{args.kind}:{dom}")
+        except Exception:
+            traffic = None
+    roof = None
+    if dom:
+        ach = stages[dom]["GBps"]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak if ach else None, "traffic": traffic,
+                "alg_bytes_per_launch": stages[dom]["alg_bytes"], "ms_per_launch": stages[dom]["ms"],
+                "peak_source": peak_src,
+                "note": f"dominant stage overall: {dom_all} "
+                        f"({stages[dom_all]['share']:.0%} of the iteration)"}
+    ach_it = alg_iter / (per_iter_ms / 1e3) / 1e9
+    roof_it = {"bound": "hbm", "achieved": ach_it, "peak": peak, "unit": "GB/s",
+               "frac": ach_it / peak, "frac_of_8TBps": ach_it / 8000.0,
+               "alg_bytes_per_iteration": alg_iter, "ms_per_iteration": per_iter_ms,
+               "model": "fused minimum (18d+1)U / (14d+1)U, SURVEY 8(d)"}
+
+    # ---- e2e through the public API with host (pinned) buffers -----------
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = run_e2e(args, P, torch, world)
+
+    line = {
+        "metric": metric_name(args), "value": value, "unit": "GDOF-it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json config generator; see DESIGN.md)",
+        "config": config_of(args), "roofline": roof, "roofline_iteration": roof_it,
+        "stages_ms_per_iteration": {k: round(v["ms"], 4) for k, v in stages.items()},
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+    }
+    return line
+
+
+def run_e2e(args, P, torch, world):
+    from paper_2508_02613_b200 import grid as G
+    from paper_2508_02613_b200.material import isotropic_material
+    from paper_2508_02613_b200.operators import make_operator, op_handle
+    from paper_2508_02613_b200.preconditioners import GreenOperator, JacobiDiagonal, Preconditioner
+    from paper_2508_02613_b200.solver import pcg
+    d, n = P["d"], P["n"]
+    grid = G.make_grid(n, (1.0,) * d)
+    mat = isotropic_material(P["lam"], P["mu"], d)
+    # density and rhs live in pinned host memory (the caller's buffers)
+    rho_h = torch.empty(P["rho"].shape, dtype=torch.float64, pin_memory=True)
+    rho_h.copy_(P["rho"])
+    rhs_h = torch.empty(P["rhs"].shape, dtype=torch.float64, pin_memory=True)
+    rhs_h.copy_(P["rhs"])
+    op = make_operator(G.ScalarField(grid, rho_h.numpy()), mat)
+    op_handle(op)  # operator assembly (density upload) is setup, as in the reference
+    green = GreenOperator(grid, mat, P["green"])
+    jac = JacobiDiagonal(grid, P["jac"]) if P["jac"] is not None else None
+    pre = Preconditioner(args.kind, green=green, jacobi=jac)
+    rhs = G.VectorField(grid, rhs_h.numpy())
+    pcg(op, rhs, pre, green, eta=-1.0, max_iter=args.iters)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        rep = pcg(op, rhs, pre, green, eta=-1.0, max_iter=args.iters)
+        _ = float(rep.solution.values[0].ravel()[0])
+    dt = time.perf_counter() - t0
+    value = world * d * n ** d * args.iters * args.e2e_steps / dt / 1e9
+    nbytes = d * n ** d * 8
+    return {"value": value, "unit": "GDOF-it/s", "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes + 8 * (args.iters + 1),
+            "api": "paper_2508_02613_b200.pcg(op, rhs, preconditioner, green) host VectorField "
+                   "(pinned), solution returned on the host"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        line = run_reference(args, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    import torch
+    import torch.distributed as dist
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ["JFFTB_DEVICE"] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = run_ours(args, rank, world)
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_single(args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,17 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
               int max_iter, double* x_out, double* history_out, int* iterations,
               int* terminated, double* wall_s);
 
+/* ---- device-side stage profile (no reference counterpart; SolveReport's
+ * wall_time, solver.py:88,139, is the reference's only timing) ----------- */
+#define JFFTB_N_STAGES 8  /* stencil, alpha, update, fft_fwd, spectral,
+                             finalize, fft_inv, pupdate */
+/* reset and enable: CUDA events are recorded between the stages of every
+ * PCG iteration of this grid, on the grid's stream */
+int jfftb_profile_start(jfftb_grid* g);
+/* stage_ms[JFFTB_N_STAGES] summed over the iterations completed since start
+ * (iterations that ran past convergence are not counted); stop != 0 disables */
+int jfftb_profile_read(jfftb_grid* g, double* stage_ms, int64_t* iterations, int stop);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,8 @@ _SIGS = {
     "jfftb_apply_precond": (C.c_int, [C.c_int, _P, _P, _P, _P, C.c_int]),
     "jfftb_pcg": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, C.c_double, C.c_int, _P,
                             _D, C.POINTER(C.c_int), C.POINTER(C.c_int), _D]),
+    "jfftb_profile_start": (C.c_int, [_P]),
+    "jfftb_profile_read": (C.c_int, [_P, _D, _I64, C.c_int]),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -159,6 +161,16 @@ class GridHandle(_Handle):
 
     def synchronize(self):
         check(load().jfftb_grid_synchronize(self.ptr))
+
+    def profile_start(self):
+        check(load().jfftb_profile_start(self.ptr))
+
+    def profile_read(self, stop: bool = True):
+        """(stage_ms[8], iterations) accumulated since profile_start."""
+        ms = np.zeros(8)
+        it = C.c_int64(0)
+        check(load().jfftb_profile_read(self.ptr, dptr(ms), C.byref(it), 1 if stop else 0))
+        return ms, it.value
 
 
 class OpHandle(_Handle):

@@ -230,6 +230,59 @@ void precond_device(int kind, jfftb_green* green, jfftb_jacobi* jac, jfftb_grid*
 void set_last_error(const std::string& m) { g_last_error = m; }
 void count_launch(int n) { g_launches += n; }
 
+void prof_mark(jfftb_grid* g) {
+  if (!g->prof) return;
+  cudaEvent_t e;
+  if (g->ev_free.empty()) {
+    JF_CUDA(cudaEventCreate(&e));
+  } else {
+    e = g->ev_free.back();
+    g->ev_free.pop_back();
+  }
+  JF_CUDA(cudaEventRecord(e, g->stream));
+  g->ev_cur.push_back(e);
+}
+
+void prof_end_iter(jfftb_grid* g) {
+  if (!g->prof) return;
+  g->ev_pending.push_back(g->ev_cur);
+  g->ev_cur.clear();
+  ++g->prof_seq;
+}
+
+// Accumulate the stage times of issued iterations whose sequence number is
+// <= real_iters (the solve's true iteration count); the stream must be idle.
+void prof_collect(jfftb_grid* g, int64_t real_iters, bool final) {
+  if (!g->prof) return;
+  size_t keep = 0;
+  std::vector<std::vector<cudaEvent_t>> rest;
+  for (auto& ev : g->ev_pending) {
+    const int64_t seq = g->prof_done_seq + 1;
+    if (seq <= real_iters && ev.size() == JFFTB_N_STAGES + 1) {
+      for (int k = 0; k < JFFTB_N_STAGES; ++k) {
+        float ms = 0.f;
+        JF_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+        g->prof_ms[k] += ms;
+      }
+      ++g->prof_iters;
+      ++g->prof_done_seq;
+      for (auto e : ev) g->ev_free.push_back(e);
+    } else if (final) {
+      for (auto e : ev) g->ev_free.push_back(e);
+    } else {
+      rest.push_back(ev);
+      ++keep;
+    }
+  }
+  g->ev_pending.swap(rest);
+  if (final) {
+    g->prof_seq = g->prof_done_seq = 0;
+    for (auto e : g->ev_cur) g->ev_free.push_back(e);
+    g->ev_cur.clear();
+  }
+  (void)keep;
+}
+
 }  // namespace jfftb
 
 using namespace jfftb;
@@ -298,6 +351,8 @@ int jfftb_grid_destroy(jfftb_grid* g) {
     if (g->fft_work) cudaFree(g->fft_work);
     if (g->partials) cudaFree(g->partials);
     if (g->dscal) cudaFree(g->dscal);
+    prof_collect(g, 0, true);
+    for (auto e : g->ev_free) cudaEventDestroy(e);
     cudaStreamDestroy(g->own_stream);
     delete g;
   });
@@ -728,6 +783,7 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
       JF_CUDA(cudaStreamSynchronize(s));
       return hs->done != 0;
     };
+    prof_collect(g, 0, true);  // drop leftovers of an aborted solve
     pcg_dispatch(kind, true, op, jac, green_pc, green_term, B);
     bool done = poll();
     // host loop: iterations are predicated on the device flag, so a few can
@@ -736,8 +792,10 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     while (!done) {
       for (int k = 0; k < batch; ++k) pcg_dispatch(kind, false, op, jac, green_pc, green_term, B);
       done = poll();
+      prof_collect(g, hs->iters, false);
       batch = std::min(batch * 2, 8);
     }
+    prof_collect(g, hs->iters, true);
     const int it = hs->iters;
     *iterations = it;
     JF_CUDA(cudaMemcpyAsync(history_out, B.hist, sizeof(double) * (it + 1),
@@ -761,6 +819,24 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     JF_CUDA(cudaStreamSynchronize(s));
     if (wall_s)
       *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int jfftb_profile_start(jfftb_grid* g) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    g->prof = true;
+    for (int k = 0; k < JFFTB_N_STAGES; ++k) g->prof_ms[k] = 0.0;
+    g->prof_iters = 0;
+  });
+}
+
+int jfftb_profile_read(jfftb_grid* g, double* stage_ms, int64_t* iterations, int stop) {
+  return guarded([&] {
+    require(g != nullptr && stage_ms != nullptr && iterations != nullptr, "null argument");
+    for (int k = 0; k < JFFTB_N_STAGES; ++k) stage_ms[k] = g->prof_ms[k];
+    *iterations = g->prof_iters;
+    if (stop) g->prof = false;
   });
 }
 

@@ -8,6 +8,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/jfftb200.h"
 
@@ -90,6 +91,15 @@ struct jfftb_grid {
   double* partials = nullptr;   // per-block partial sums
   int partials_cap = 0;
   double* dscal = nullptr;      // small device scalar scratch
+  // stage profile (jfftb_profile_*)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<cudaEvent_t> ev_cur;                  // events of the iteration being issued
+  std::vector<std::vector<cudaEvent_t>> ev_pending;  // issued iterations, oldest first
+  int64_t prof_seq = 0;       // iterations issued in the current solve
+  int64_t prof_done_seq = 0;  // iterations of the current solve already collected
+  double prof_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t prof_iters = 0;
 };
 
 struct jfftb_op {
@@ -298,6 +308,11 @@ struct PcgBuffers {
 };
 void pcg_dispatch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
                   jfftb_green* gterm, const PcgBuffers& B);
+
+// stage profile hooks (api.cu); no-ops unless jfftb_profile_start was called
+void prof_mark(jfftb_grid* g);         // event at a stage boundary
+void prof_end_iter(jfftb_grid* g);     // close the iteration being issued
+void prof_collect(jfftb_grid* g, int64_t real_iters, bool final);
 void launch_pcg_spectral(const Geom& g, cudaStream_t s, int mode, const double* gpc,
                          const double* gterm, double2* spec, const PcgState* st,
                          double* partials);

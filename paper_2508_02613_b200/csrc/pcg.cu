@@ -176,19 +176,17 @@ static void pcg_precond_phase(jfftb_grid* g, jfftb_jacobi* jac, jfftb_green* gpc
   update_kernel<KIND, INIT><<<kRedBlocks, 256, 0, s>>>(n, B.st, B.x, r, B.p, B.kp, dinv, sz,
                                                        B.upart);
   JF_LAUNCHED();
-  if (KIND == JFFTB_PC_GREEN_JACOBI) {
-    run_fwd_fft(g, 1, B.rs, B.spec);
-    launch_pcg_spectral(geo, s, 1, gpc->blocks, gterm->blocks, B.spec, B.st, B.spart);
-  } else if (KIND == JFFTB_PC_GREEN) {
-    run_fwd_fft(g, 0, r, B.spec);
-    launch_pcg_spectral(geo, s, 0, gpc->blocks, gterm->blocks, B.spec, B.st, B.spart);
-  } else {
-    run_fwd_fft(g, 0, r, B.spec);
-    launch_pcg_spectral(geo, s, 2, gterm->blocks, gterm->blocks, B.spec, B.st, B.spart);
-  }
+  if (!INIT) prof_mark(g);
+  const int mode = KIND == JFFTB_PC_GREEN_JACOBI ? 1 : (KIND == JFFTB_PC_GREEN ? 0 : 2);
+  run_fwd_fft(g, KIND == JFFTB_PC_GREEN_JACOBI, B.rs, B.spec);
+  if (!INIT) prof_mark(g);
+  launch_pcg_spectral(geo, s, mode, (mode == 2 ? gterm : gpc)->blocks, gterm->blocks, B.spec,
+                      B.st, B.spart);
+  if (!INIT) prof_mark(g);
   finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, kRedBlocks, B.upart, kRedBlocks,
                                                  B.hist);
   JF_LAUNCHED();
+  if (!INIT) prof_mark(g);
   const double* zsrc = r;
   if (KIND == JFFTB_PC_GREEN_JACOBI) {
     run_inv_fft(g, B.spec + geo.d * geo.Nh, sz);
@@ -199,8 +197,13 @@ static void pcg_precond_phase(jfftb_grid* g, jfftb_jacobi* jac, jfftb_green* gpc
   } else if (KIND == JFFTB_PC_JACOBI) {
     zsrc = sz;
   }
+  if (!INIT) prof_mark(g);
   pupdate_kernel<KIND, INIT><<<grid_n(n), 256, 0, s>>>(n, B.st, B.p, zsrc, dinv);
   JF_LAUNCHED();
+  if (!INIT) {
+    prof_mark(g);
+    prof_end_iter(g);
+  }
 }
 
 template <int KIND>
@@ -208,9 +211,12 @@ static void pcg_iteration(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
                           jfftb_green* gterm, const PcgBuffers& B) {
   jfftb_grid* g = op->grid;
   cudaStream_t s = g->stream;
+  prof_mark(g);
   launch_stencil(g->geo, s, ST_K, B.p, op->rho, op->lambda0, op->mu0, nullptr, B.kp, B.kpart);
+  prof_mark(g);
   alpha_kernel<<<1, 1024, 0, s>>>(B.st, B.kpart, B.kcount);
   JF_LAUNCHED();
+  prof_mark(g);
   pcg_precond_phase<KIND, false>(g, jac, gpc, gterm, B);
 }
 

@@ -115,6 +115,36 @@ def crack_discs(n: int = 512, count: int = 64, ell: float = 4.0,
     return out
 
 
+def crack_discs_device(n: int = 512, count: int = 64, ell: float = 4.0, emin: float = 1e-4,
+                       seed: int = 0, device="cuda", out=None):
+    """Device (torch) version of :func:`crack_discs` with the same seeded
+    geometry, for bench-size grids; returns an (n, n, n) float64 tensor."""
+    import torch
+    centres, normals, radii = crack_discs_params(n, count, seed=seed)
+    ax = torch.arange(n, dtype=torch.float64, device=device) + 0.5
+    if out is None:
+        out = torch.empty((n, n, n), dtype=torch.float64, device=device)
+    chunk = max(1, min(n, (1 << 24) // (n * n)))
+    for i0 in range(0, n, chunk):
+        x0 = ax[i0:i0 + chunk]
+        dmin = torch.full((len(x0), n, n), float("inf"), dtype=torch.float64, device=device)
+        for c, nr, r in zip(centres, normals, radii):
+            v0 = x0 - c[0]
+            v0 = (v0 - n * torch.round(v0 / n))[:, None, None]
+            v1 = ax - c[1]
+            v1 = (v1 - n * torch.round(v1 / n))[None, :, None]
+            v2 = ax - c[2]
+            v2 = (v2 - n * torch.round(v2 / n))[None, None, :]
+            hgt = v0 * float(nr[0]) + v1 * float(nr[1]) + v2 * float(nr[2])
+            rad = torch.sqrt(torch.clamp(v0 * v0 + v1 * v1 + v2 * v2 - hgt * hgt, min=0.0))
+            dist = torch.where(rad <= float(r), hgt.abs(),
+                               torch.sqrt(hgt * hgt + (rad - float(r)) ** 2))
+            torch.minimum(dmin, dist, out=dmin)
+        phi = torch.exp(-dmin / ell)
+        out[i0:i0 + chunk] = (1.0 - phi) ** 2 + emin
+    return out
+
+
 def mandel_shear(d: int, i: int, j: int, gamma: float = 0.5) -> np.ndarray:
     """Mandel vector of the symmetric strain with eps_ij = eps_ji = gamma."""
     from .grid import mandel_index
