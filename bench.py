@@ -225,6 +225,7 @@ def build_problem(args, torch, dev):
         rho = torch.from_numpy(ms.bernoulli_smoothed(n, 20, 1e4, 0)).to(dev)
     gh = N.GridHandle(d, shape, (1.0,) * d, device=torch.cuda.current_device())
     gh.set_stream(torch.cuda.current_stream().cuda_stream)
+    N.register_grid(gh)  # the public-API (e2e) leg shares this context
     op = N.OpHandle(gh, rho.data_ptr(), lam, mu, where=N.DEVICE)
     green = N.GreenHandle(gh, lam, mu)
     jac = N.JacobiHandle(op) if args.kind == "green-jacobi" else None

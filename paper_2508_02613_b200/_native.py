@@ -219,5 +219,13 @@ def grid_handle(d: int, n, lengths) -> GridHandle:
     return h
 
 
+def register_grid(h: GridHandle) -> None:
+    """Make an explicitly created grid context the one the Python API uses
+    for its (d, n, lengths) (e.g. a context bound to a torch stream)."""
+    key = (os.getpid(), h.d, tuple(int(k) for k in h.n), tuple(float(l) for l in h.lengths),
+           device_id())
+    _grid_cache[key] = h
+
+
 def launch_count(reset: bool = False) -> int:
     return int(load().jfftb_launch_count(1 if reset else 0))

@@ -2,6 +2,7 @@
 // staging, preconditioner setup, and the PCG driver loop.
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -186,6 +187,48 @@ int read_flag(jfftb_grid* g, int* dflag) {
   return h;
 }
 
+// PCG workspace, allocated once per grid (and regrown only for a longer
+// history): x, [r; s], p, Kp, 2d half spectra, state, history, partials
+PcgBuffers pcg_workspace(jfftb_grid* g, int kcount, int max_iter) {
+  const Geom& geo = g->geo;
+  const int64_t n = geo.d * geo.N;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t need_hist = sizeof(double) * (size_t)(max_iter + 1);
+  const int64_t nspec = std::max<int64_t>(geo.Nh, spec_elems(g));
+  const int sblocks = std::max(kRedBlocks, kFusedMaxBlocks);
+  const size_t fixed = al(sizeof(double) * n) * 3 + al(sizeof(double) * 2 * n) +
+                       al(sizeof(double2) * 2 * geo.d * nspec) + al(sizeof(PcgState)) +
+                       al(sizeof(double) * (kcount + 2 * sblocks + kRedBlocks));
+  const size_t total = fixed + al(need_hist);
+  if (g->ws_bytes < total) {
+    if (g->ws) JF_CUDA(cudaFree(g->ws));
+    g->ws = nullptr;
+    g->ws_bytes = 0;
+    JF_CUDA(cudaMalloc(&g->ws, total + al(sizeof(double) * 1024)));  // history headroom
+    g->ws_bytes = total + al(sizeof(double) * 1024);
+  }
+  if (!g->ws_host) JF_CUDA(cudaMallocHost(&g->ws_host, sizeof(PcgState)));
+  char* p = static_cast<char*>(g->ws);
+  auto take = [&](size_t b) {
+    char* q = p;
+    p += al(b);
+    return q;
+  };
+  PcgBuffers B{};
+  B.x = (double*)take(sizeof(double) * n);
+  B.rs = (double*)take(sizeof(double) * 2 * n);
+  B.p = (double*)take(sizeof(double) * n);
+  B.kp = (double*)take(sizeof(double) * n);
+  B.spec = (double2*)take(sizeof(double2) * 2 * geo.d * nspec);
+  B.st = (PcgState*)take(sizeof(PcgState));
+  B.kpart = (double*)take(sizeof(double) * (kcount + 2 * sblocks + kRedBlocks));
+  B.spart = B.kpart + kcount;
+  B.upart = B.spart + 2 * sblocks;
+  B.kcount = kcount;
+  B.hist = (double*)p;
+  return B;
+}
+
 // precondition r (device, d*N) into out (device) for kind (-1 = jacobi half)
 void precond_device(int kind, jfftb_green* green, jfftb_jacobi* jac, jfftb_grid* g,
                     const double* r, double* out) {
@@ -205,6 +248,14 @@ void precond_device(int kind, jfftb_green* green, jfftb_jacobi* jac, jfftb_grid*
   } else if (kind == JFFTB_PC_GREEN || kind == JFFTB_PC_GREEN_JACOBI) {
     need_green();
     if (kind == JFFTB_PC_GREEN_JACOBI) need_jac();
+    if (g->fused) {
+      DevBuf spec(sizeof(double2) * geo.d * spec_elems(g));
+      fused_precond_apply(geo, s, green->blocks,
+                          kind == JFFTB_PC_GREEN_JACOBI ? jac->inv_sqrt : nullptr, r, out,
+                          spec.as<double2>(), g->twiddle);
+      JF_CUDA(cudaStreamSynchronize(s));  // spec is freed on return
+      return;
+    }
     ensure_plans(g);
     DevBuf spec(sizeof(double2) * geo.d * geo.Nh);
     DevBuf tmp(kind == JFFTB_PC_GREEN_JACOBI ? sizeof(double) * n : 0);
@@ -334,6 +385,14 @@ int jfftb_grid_create(int d, const int64_t* n, const double* lengths, int device
     }
     g->stream = g->own_stream;
     JF_CUDA(cudaMalloc(&g->dscal, 64 * sizeof(double)));
+    // JFFTB_DISABLE_FUSED=1 forces the cuFFT spectral path (A/B testing)
+    const char* nofuse = std::getenv("JFFTB_DISABLE_FUSED");
+    g->fused = fused_supported(geo) && !(nofuse && nofuse[0] == '1');
+    if (g->fused) {
+      JF_CUDA(cudaMalloc(&g->twiddle, sizeof(double2) * kTwiddleN));
+      launch_twiddles(g->own_stream, g->twiddle);
+      JF_CUDA(cudaStreamSynchronize(g->own_stream));
+    }
     *out = g;
   });
 }
@@ -351,6 +410,9 @@ int jfftb_grid_destroy(jfftb_grid* g) {
     if (g->fft_work) cudaFree(g->fft_work);
     if (g->partials) cudaFree(g->partials);
     if (g->dscal) cudaFree(g->dscal);
+    if (g->ws) cudaFree(g->ws);
+    if (g->ws_host) cudaFreeHost(g->ws_host);
+    if (g->twiddle) cudaFree(g->twiddle);
     prof_collect(g, 0, true);
     for (auto e : g->ev_free) cudaEventDestroy(e);
     cudaStreamDestroy(g->own_stream);
@@ -584,12 +646,13 @@ int jfftb_green_create(jfftb_grid* g, double lambda_ref, double mu_ref, jfftb_gr
     gr->lambda_ref = lambda_ref;
     gr->mu_ref = mu_ref;
     const int np = green_planes(d);
-    if (cudaMalloc(&gr->blocks, sizeof(double) * np * geo.Nh) != cudaSuccess) {
+    const int64_t nfreq = spec_elems(g);
+    if (cudaMalloc(&gr->blocks, sizeof(double) * np * nfreq) != cudaSuccess) {
       delete gr;
       throw Error(JFFTB_ECUDA, "cudaMalloc failed for Green blocks");
     }
     launch_green_setup(geo, g->stream, resp.as<double>(), m[0] | (m[1] << 8) | (m[2] << 16),
-                       gr->blocks);
+                       gr->blocks, g->fused ? 1 : 0, nfreq);
     JF_CUDA(cudaStreamSynchronize(g->stream));
     *out = gr;
   });
@@ -612,21 +675,39 @@ int jfftb_green_export_blocks(jfftb_green* green, double* out) {
     DeviceGuard dg(g->device);
     const Geom& geo = g->geo;
     const int d = geo.d, np = green_planes(d);
-    std::vector<double> packed((size_t)np * geo.Nh);
-    JF_CUDA(cudaMemcpyAsync(packed.data(), green->blocks, sizeof(double) * np * geo.Nh,
+    const int64_t nfreq = spec_elems(g);
+    std::vector<double> packed((size_t)np * nfreq);
+    JF_CUDA(cudaMemcpyAsync(packed.data(), green->blocks, sizeof(double) * np * nfreq,
                             cudaMemcpyDeviceToHost, g->stream));
     JF_CUDA(cudaStreamSynchronize(g->stream));
     for (int64_t f = 0; f < geo.Nh; ++f) {
       double* o = out + f * 2 * d * d;
+      // numpy order (last axis halved); the fused layout halves axis 0, so the
+      // other half is reached through G(-q) = conj G(q)
+      int64_t src = f;
+      double conj = 1.0;
+      if (g->fused) {
+        int q[3] = {0, 0, 0};
+        int64_t rem = f;
+        q[d - 1] = (int)(rem % geo.nh);
+        rem /= geo.nh;
+        for (int a = d - 2; a >= 0; --a) { q[a] = (int)(rem % geo.n[a]); rem /= geo.n[a]; }
+        if (2 * q[0] > geo.n[0]) {
+          for (int a = 0; a < d; ++a) q[a] = (geo.n[a] - q[a]) % geo.n[a];
+          conj = -1.0;
+        }
+        src = q[0];
+        for (int a = 1; a < d; ++a) src = src * geo.n[a] + q[a];
+      }
       for (int a = 0; a < d; ++a) {
-        o[2 * (a * d + a)] = packed[a * geo.Nh + f];
+        o[2 * (a * d + a)] = packed[a * nfreq + src];
         o[2 * (a * d + a) + 1] = 0.0;
       }
       int k = 0;
       for (int a = 0; a < d; ++a)
         for (int b = a + 1; b < d; ++b, ++k) {
-          const double re = packed[(d + 2 * k) * geo.Nh + f];
-          const double im = packed[(d + 2 * k + 1) * geo.Nh + f];
+          const double re = packed[(d + 2 * k) * nfreq + src];
+          const double im = conj * packed[(d + 2 * k + 1) * nfreq + src];
           o[2 * (a * d + b)] = re;
           o[2 * (a * d + b) + 1] = im;
           o[2 * (b * d + a)] = re;
@@ -743,41 +824,24 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     cudaStream_t s = g->stream;
     ensure_plans(g);
     const int64_t n = geo.d * geo.N;
-    DevBuf tin;
-    const double* drhs = stage_in(g, rhs, n, where, tin);
+    require(rhs != nullptr, "null right-hand side");
+    require(where == JFFTB_HOST || where == JFFTB_DEVICE, "where must be HOST or DEVICE");
 
-    // workspace
+    // workspace: one allocation cached on the grid and reused by every solve
     const int kcount = stencil_blocks(geo);
-    DevBuf bx(sizeof(double) * n), brs(sizeof(double) * 2 * n), bp(sizeof(double) * n),
-        bkp(sizeof(double) * n), bspec(sizeof(double2) * 2 * geo.d * geo.Nh),
-        bst(sizeof(PcgState)), bhist(sizeof(double) * (max_iter + 1)),
-        bpart(sizeof(double) * (kcount + 2 * kRedBlocks + kRedBlocks));
-    PcgBuffers B{};
-    B.x = bx.as<double>();
-    B.rs = brs.as<double>();
-    B.p = bp.as<double>();
-    B.kp = bkp.as<double>();
-    B.spec = bspec.as<double2>();
-    B.st = bst.as<PcgState>();
-    B.hist = bhist.as<double>();
-    B.kpart = bpart.as<double>();
-    B.spart = B.kpart + kcount;
-    B.upart = B.spart + 2 * kRedBlocks;
-    B.kcount = kcount;
+    PcgBuffers B = pcg_workspace(g, kcount, max_iter);
+    PcgState* hs = g->ws_host;
 
     PcgState h0{};
     h0.eta = eta;
     h0.max_iter = max_iter;
-    JF_CUDA(cudaMemcpyAsync(B.st, &h0, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+    *hs = h0;
+    JF_CUDA(cudaMemcpyAsync(B.st, hs, sizeof(PcgState), cudaMemcpyHostToDevice, s));
     JF_CUDA(cudaMemsetAsync(B.x, 0, sizeof(double) * n, s));
-    JF_CUDA(cudaMemcpyAsync(B.rs, drhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-
-    PcgState* hs = nullptr;
-    JF_CUDA(cudaMallocHost(&hs, sizeof(PcgState)));
-    struct HostFree {
-      PcgState* p;
-      ~HostFree() { cudaFreeHost(p); }
-    } hf{hs};
+    JF_CUDA(cudaMemcpyAsync(B.rs, rhs, sizeof(double) * n,
+                            where == JFFTB_HOST ? cudaMemcpyHostToDevice
+                                                : cudaMemcpyDeviceToDevice,
+                            s));
     auto poll = [&]() {
       JF_CUDA(cudaMemcpyAsync(hs, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       JF_CUDA(cudaStreamSynchronize(s));

@@ -73,6 +73,7 @@ struct PcgState {
   int iters;    // search-direction updates so far
   int status;   // JFFTB_OK / JFFTB_ENONFINITE / JFFTB_ECURVATURE
   int max_iter;
+  int xupd;     // fused path: this iteration's alpha is valid (x += alpha p pending)
 };
 
 }  // namespace jfftb
@@ -91,6 +92,13 @@ struct jfftb_grid {
   double* partials = nullptr;   // per-block partial sums
   int partials_cap = 0;
   double* dscal = nullptr;      // small device scalar scratch
+  // fused spectral path (fused.cu): power-of-two grids, 16 <= n <= 2048
+  bool fused = false;
+  double2* twiddle = nullptr;   // exp(-2 pi i j / 4096)
+  // cached PCG workspace (api.cu pcg_workspace)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  jfftb::PcgState* ws_host = nullptr;  // pinned mirror of the device state
   // stage profile (jfftb_profile_*)
   bool prof = false;
   std::vector<cudaEvent_t> ev_free;
@@ -294,8 +302,10 @@ int green_planes(int d);
 void launch_green_apply(const Geom& g, cudaStream_t s, const double* blocks,
                         const double2* in, double2* out, int ncomp_batches);
 // resp: d x d x prod(m) impulse responses on the small grid m (packed m0|m1<<8|m2<<16)
+// layout 0: numpy rfftn order (last axis halved), nfreq = Nh; layout 1:
+// fused.cu order (axis 0 halved), nfreq = fused_spec_elems
 void launch_green_setup(const Geom& g, cudaStream_t s, const double* resp, int m,
-                        double* blocks);
+                        double* blocks, int layout, int64_t nfreq);
 
 // PCG (pcg.cu)
 struct PcgBuffers {
@@ -308,6 +318,33 @@ struct PcgBuffers {
 };
 void pcg_dispatch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
                   jfftb_green* gterm, const PcgBuffers& B);
+
+// fused spectral path (fused.cu)
+bool fused_supported(const Geom& g);
+int64_t fused_spec_elems(const Geom& g);   // complex elements per spectral component
+constexpr int kFusedMaxBlocks = 148 * 4 * 8;  // bound on pass-C partial pairs
+constexpr int kTwiddleN = 4096;               // twiddle table entries (fft.cuh kTwN)
+// complex elements per spectral component of whichever layout the grid uses
+inline int64_t spec_elems(const jfftb_grid* g) {
+  return g->fused ? fused_spec_elems(g->geo) : g->geo.Nh;
+}
+void launch_twiddles(cudaStream_t s, double2* tw);
+void fused_precond_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
+                         const double* dinv, const double* r, double* out, double2* spec,
+                         const double2* tw);
+enum { FUSED_APPLY = 0, FUSED_INIT = 1, FUSED_ITER = 2 };
+void fused_stage_A(const Geom& geo, cudaStream_t s, int F, int mode, const PcgState* st,
+                   double* r, const double* kp, const double* dinv, double2* spec,
+                   const double2* tw);
+void fused_stage_B(const Geom& geo, cudaStream_t s, bool inv, const PcgState* st,
+                   double2* spec, int ncomp, const double2* tw);
+int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const PcgState* st,
+                  const double* gpc, const double* gterm, double2* spec, double* partials,
+                  const double2* tw);
+void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
+                   const double2* zspec, const double* dinv, double* p, double* x,
+                   const double2* tw);
+int64_t fused_component_stride(const Geom& geo);
 
 // stage profile hooks (api.cu); no-ops unless jfftb_profile_start was called
 void prof_mark(jfftb_grid* g);         // event at a stage boundary

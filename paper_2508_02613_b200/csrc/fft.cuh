@@ -1,0 +1,183 @@
+// Device FFT building blocks for the fused spectral passes (fused.cu).
+//
+// cta_fft<L, NSEQ, NT, INV> transforms NSEQ sequences of length L (power of
+// two, 2..2048) held in shared memory, element k of sequence q at
+// buf[q * qs + k * ks], with a Stockham autosort radix-8 (+ one radix-2/4)
+// schedule.  Every stage reads all its butterfly inputs into registers,
+// barriers, and writes in place, so no ping-pong buffer is needed; NT threads
+// share the NSEQ * L / R butterflies of a stage.  Twiddles come from one
+// 4096-entry table of exp(-2 pi i j / 4096) (fp64, built once per grid).
+// Forward = numpy's unnormalised exp(-i...) convention; INV = exp(+i...)
+// without the 1/L factor (folded into the spectral multiply).
+#pragma once
+
+#include "common.cuh"
+
+namespace jfftb {
+
+constexpr int kTwN = 4096;
+
+// Ampere+ asynchronous global -> shared copies (LDGSTS), used to prefetch the
+// next tile while the current one is transformed
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+__device__ __forceinline__ double2 mul_mi(double2 a) {
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft2(double2& a, double2& b) {
+  const double2 t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& v0, double2& v1, double2& v2, double2& v3) {
+  const double2 t0 = cadd(v0, v2), t1 = csub(v0, v2);
+  const double2 t2 = cadd(v1, v3), t3 = mul_mi<INV>(csub(v1, v3));
+  v0 = cadd(t0, t2);
+  v2 = csub(t0, t2);
+  v1 = cadd(t1, t3);
+  v3 = csub(t1, t3);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft8(double2 (&v)[8]) {
+  constexpr double h = 0.70710678118654752440;
+  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  // W8^1 = h(1 -+ i), W8^2 = -+i, W8^3 = h(-1 -+ i)
+  const double2 w1o1 = INV ? make_double2(h * (o1.x - o1.y), h * (o1.x + o1.y))
+                           : make_double2(h * (o1.x + o1.y), h * (o1.y - o1.x));
+  const double2 w2o2 = mul_mi<INV>(o2);
+  const double2 w3o3 = INV ? make_double2(-h * (o3.x + o3.y), h * (o3.x - o3.y))
+                           : make_double2(h * (o3.y - o3.x), -h * (o3.x + o3.y));
+  v[0] = cadd(e0, o0);
+  v[4] = csub(e0, o0);
+  v[1] = cadd(e1, w1o1);
+  v[5] = csub(e1, w1o1);
+  v[2] = cadd(e2, w2o2);
+  v[6] = csub(e2, w2o2);
+  v[3] = cadd(e3, w3o3);
+  v[7] = csub(e3, w3o3);
+}
+
+// radix of stage s for length L: radix-8 stages first, one trailing 2 or 4
+__host__ __device__ constexpr int fft_nstages(int L) {
+  int s = 0;
+  while (L >= 8) { L /= 8; ++s; }
+  return s + (L > 1 ? 1 : 0);
+}
+__host__ __device__ constexpr int fft_radix(int L, int s) {
+  int full = 0, r = L;
+  while (r >= 8) { r /= 8; ++full; }
+  return s < full ? 8 : r;
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dftR(double2 (&v)[8]) {
+  if (R == 8) dft8<INV>(v);
+  else if (R == 4) dft4<INV>(v[0], v[1], v[2], v[3]);
+  else if (R == 2) dft2<INV>(v[0], v[1]);
+}
+
+// element k of a sequence sits at pidx(k) * ks: PAD inserts one slot every 8
+// elements so that the radix-8 stride patterns of contiguous (ks = 1) rows
+// stay free of shared-memory bank conflicts
+template <int PAD>
+__device__ __forceinline__ int pidx(int k) {
+  return PAD ? k + k / PAD : k;
+}
+template <int PAD>
+__host__ __device__ constexpr int padded_len(int L) {
+  return PAD ? L + L / PAD : L;
+}
+
+// QFAST: consecutive threads take consecutive sequences (layouts with qs = 1,
+// sequences interleaved); otherwise consecutive butterflies of one sequence
+template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, int S, int NS>
+__device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
+                                              const double2* __restrict__ tw) {
+  if constexpr (S < fft_nstages(L)) {
+    constexpr int R = fft_radix(L, S);
+    constexpr int NB = L / R;            // butterflies per sequence
+    constexpr int B = NSEQ * NB;         // butterflies per stage
+    constexpr int PER = (B + NT - 1) / NT;
+    double2 v[PER][8];
+    int qq[PER], jj[PER];
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int b = threadIdx.x + m * NT;
+      qq[m] = QFAST ? b % NSEQ : b / NB;
+      jj[m] = QFAST ? b / NSEQ : b % NB;
+      if (B % NT == 0 || b < B) {
+        const double2* src = buf + qq[m] * qs;
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[m][t] = src[pidx<PAD>(jj[m] + t * NB) * ks];
+        if (NS > 1) {
+          const int base = (jj[m] % NS) * (kTwN / (NS * R));
+#pragma unroll
+          for (int t = 1; t < R; ++t) {
+            const double2 w = __ldg(tw + ((base * t) & (kTwN - 1)));
+            v[m][t] = INV ? cmulc(v[m][t], w) : cmul(v[m][t], w);
+          }
+        }
+        dftR<R, INV>(v[m]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int b = threadIdx.x + m * NT;
+      if (B % NT == 0 || b < B) {
+        const int j = jj[m];
+        double2* dst = buf + qq[m] * qs;
+        const int o = (j / NS) * NS * R + (j % NS);
+#pragma unroll
+        for (int t = 0; t < R; ++t) dst[pidx<PAD>(o + t * NS) * ks] = v[m][t];
+      }
+    }
+    __syncthreads();
+    cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, S + 1, NS * R>(buf, ks, qs, tw);
+  }
+}
+
+// Transform NSEQ sequences in smem in place.  Caller must __syncthreads()
+// before (data written) -- this routine ends with a barrier.
+template <int L, int NSEQ, int NT, bool INV, bool QFAST = true, int PAD = 0>
+__device__ __forceinline__ void cta_fft(double2* buf, int ks, int qs,
+                                        const double2* __restrict__ tw) {
+  cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, 0, 1>(buf, ks, qs, tw);
+}
+
+// exp(-2 pi i j / 4096), j < 4096
+void launch_twiddles(cudaStream_t s, double2* tw);
+
+}  // namespace jfftb

@@ -1,0 +1,655 @@
+// Fused spectral passes: the Green / Green-Jacobi preconditioner and the PCG
+// vector updates with hand-written fp64 FFTs (replaces preconditioners.py:
+// 83-94, 122-136 and the axpys of solver.py:119-136 on power-of-two grids).
+//
+// Internal spectrum layout ("axis-0 half spectrum"): spec[c][k0][i1][i2],
+// k0 = 0..n0/2 (the real-to-complex axis is the slowest one), full extent on
+// the other axes, so the last transform before the Green block solve runs
+// along contiguous rows.  Per PCG iteration (d = 3, green-jacobi):
+//
+//   A   axis-0 R2C of r and s = D^-1/2 r, fused with r -= alpha Kp   (18 U)
+//   B   axis-1 complex FFT of the 6 half spectra, in place            (12 U)
+//   C   axis-2 FFT + Green block solve + <r,Gr>, <s,Gs> + axis-2 iFFT (13.5 U)
+//   B'  axis-1 inverse FFT of the 3 z^ spectra                        ( 6 U)
+//   I   axis-0 C2R fused with x += alpha p, p = D^-1/2 z + beta p     (18 U)
+//
+// (U = 8 N bytes.)  Every pass is one read and one write of its data; the
+// forward and inverse transforms along the last axis share one pass with the
+// block solve between them.  All passes are predicated on the device PCG
+// state, so iterations can be queued / graph-captured without host syncs.
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace jfftb {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void twiddle_kernel(double2* tw) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < kTwN) {
+    double s, c;
+    sincospi(-2.0 * (double)j / (double)kTwN, &s, &c);
+    tw[j] = make_double2(c, s);
+  }
+}
+
+enum FMode { FM_APPLY = FUSED_APPLY, FM_INIT = FUSED_INIT, FM_ITER = FUSED_ITER, FM_QUAD = 3 };
+
+struct FGeom {
+  int d, n0, nlast;
+  int M0, K0;      // n0 / 2, n0 / 2 + 1
+  int64_t PS;      // elements per axis-0 plane (= N / n0)
+  int64_t CS;      // complex elements per spectral component (= K0 * PS)
+  int64_t N;
+  int n1;          // d = 3: axis-1 extent
+};
+
+constexpr int tw_a(int M) { return M >= 512 ? 4 : 8; }
+constexpr int tw_b(int L) { return L >= 1024 ? 4 : 8; }
+// one radix-8 butterfly per thread where possible (<= 512 threads)
+constexpr int nt_for(int butterflies) {
+  return butterflies >= 512 ? 512 : (butterflies <= 64 ? 64 : (butterflies + 31) / 32 * 32);
+}
+
+// ---------------------------------------------------------------------------
+// pass A: axis-0 real-to-complex of r (and s = D^-1/2 r), fused with the
+// residual update r -= alpha Kp (FM_ITER).  F = 1 (green) or 2 (green-jacobi).
+// FM_APPLY: src = the vector to precondition (not written), F = 1, s-only when
+// `dinv` is given (green-jacobi) else r-only.
+// ---------------------------------------------------------------------------
+template <int M, int F, int MODE>
+__global__ void __launch_bounds__(nt_for(F* tw_a(M) * M / 8))
+    passA(FGeom g, const PcgState* __restrict__ st, double* __restrict__ r,
+          const double* __restrict__ kp, const double* __restrict__ dinv,
+          double2* __restrict__ spec, const double2* __restrict__ tw) {
+  constexpr int TW = tw_a(M), FTW = F * TW;
+  constexpr int NT = nt_for(F * TW * M / 8);
+  extern __shared__ double2 sbuf[];  // [k][f * TW + col], k < M
+  if (MODE != FM_APPLY && st->done) return;
+  const int c = blockIdx.y;
+  const int64_t col0 = (int64_t)blockIdx.x * TW;
+  const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
+  double* rc = r + c * g.N;
+  const double* kc = kp ? kp + c * g.N : nullptr;
+  const double* dc = dinv ? dinv + c * g.N : nullptr;
+  // Stage the raw rows of r, Kp and D^-1/2 (2M x TW doubles each) with
+  // cp.async (full memory-level parallelism, no registers held), pull each
+  // thread's values into registers, then reuse the staging area for the packed
+  // complex tile.
+  double* raw = reinterpret_cast<double*>(sbuf);  // [array][i0][col]
+  constexpr int RAWN = 2 * M * TW;
+  const bool use_k = MODE == FM_ITER;
+  const bool use_d = MODE == FM_APPLY ? dc != nullptr : F == 2;
+  for (int e = threadIdx.x; e < RAWN / 2; e += NT) {  // 16-byte pairs
+    const int i0 = (2 * e) / TW, col = (2 * e) % TW;
+    const int64_t gi = (int64_t)i0 * g.PS + col0 + col;
+    cpa16(raw + 2 * e, rc + gi);
+    if (use_k) cpa16(raw + RAWN + 2 * e, kc + gi);
+    if (use_d) cpa16(raw + 2 * RAWN + 2 * e, dc + gi);
+  }
+  cpa_commit();
+  cpa_wait<0>();
+  __syncthreads();
+  constexpr int PE = M * TW / NT;
+  static_assert(PE * NT == M * TW, "pass A tiling");
+  double v0[PE], v1[PE], s0[PE], s1[PE];
+#pragma unroll
+  for (int j = 0; j < PE; ++j) {
+    const int e = threadIdx.x + j * NT;
+    const int m = e / TW, col = e % TW;
+    const int l0 = (2 * m) * TW + col, l1 = l0 + TW;
+    double x0 = raw[l0], x1 = raw[l1];
+    if (use_k) {
+      x0 = x0 - alpha * raw[RAWN + l0];
+      x1 = x1 - alpha * raw[RAWN + l1];
+      const int64_t gi = (int64_t)(2 * m) * g.PS + col0 + col;
+      rc[gi] = x0;
+      rc[gi + g.PS] = x1;
+    }
+    if (use_d) {
+      s0[j] = raw[2 * RAWN + l0] * x0;
+      s1[j] = raw[2 * RAWN + l1] * x1;
+    }
+    if (MODE == FM_APPLY && use_d) { x0 = s0[j]; x1 = s1[j]; }
+    v0[j] = x0;
+    v1[j] = x1;
+  }
+  __syncthreads();  // the staging area becomes the packed tile
+#pragma unroll
+  for (int j = 0; j < PE; ++j) {
+    const int e = threadIdx.x + j * NT;
+    const int m = e / TW, col = e % TW;
+    sbuf[m * FTW + col] = make_double2(v0[j], v1[j]);
+    if (F == 2) sbuf[m * FTW + TW + col] = make_double2(s0[j], s1[j]);
+  }
+  __syncthreads();
+  cta_fft<M, FTW, NT, false>(sbuf, FTW, 1, tw);
+  // unpack the packed half-length transform into X[k], k = 0..M
+  constexpr int TWS = kTwN / (2 * M);
+  for (int e = threadIdx.x; e < (M + 1) * FTW; e += NT) {
+    const int k = e / FTW, q = e % FTW;
+    const double2 zk = sbuf[(k % M) * FTW + q];
+    const double2 zc = cconj(sbuf[((M - k) % M) * FTW + q]);
+    const double2 fe = cscale(cadd(zk, zc), 0.5);
+    const double2 fo = cscale(csub(zk, zc), 0.5);                   // = i Fo
+    const double2 w = __ldg(tw + ((k * TWS) & (kTwN - 1)));         // e^{-2 pi i k / n0}
+    const double2 x = cadd(fe, cmul(w, mul_mi<false>(fo)));  // Fe + w Fo, Fo = -i fo
+    const int f = q / TW, col = q % TW;
+    spec[(f * g.d + c) * g.CS + (int64_t)k * g.PS + col0 + col] = x;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pass B: complex FFT along axis 1 (d = 3), in place, components
+// [comp0, comp0 + gridDim.z)
+// ---------------------------------------------------------------------------
+template <int L, bool INV, bool PRED>
+__global__ void __launch_bounds__(nt_for(tw_b(L) * L / 8))
+    passB(FGeom g, const PcgState* __restrict__ st, double2* __restrict__ spec, int comp0,
+          int nlast, const double2* __restrict__ tw) {
+  constexpr int TW = tw_b(L);
+  constexpr int NT = nt_for(TW * L / 8);
+  extern __shared__ double2 sbuf[];  // [i1][col]
+  if (PRED && st->done) return;
+  const int c = comp0 + blockIdx.z;
+  const int k0 = blockIdx.y;
+  const int64_t col0 = (int64_t)blockIdx.x * TW;
+  double2* base = spec + c * g.CS + (int64_t)k0 * g.PS + col0;
+  for (int e = threadIdx.x; e < L * TW; e += NT) {
+    const int i = e / TW, col = e % TW;
+    cpa16(sbuf + e, base + (int64_t)i * nlast + col);
+  }
+  cpa_commit();
+  cpa_wait<0>();
+  __syncthreads();
+  cta_fft<L, TW, NT, INV>(sbuf, TW, 1, tw);
+  for (int e = threadIdx.x; e < L * TW; e += NT) {
+    const int i = e / TW, col = e % TW;
+    base[(int64_t)i * nlast + col] = sbuf[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pass C: last-axis FFT of every row of the listed spectra, Green block solve
+// (z^ = G s^ / N) with the Parseval quadratic forms, inverse last-axis FFT of
+// z^, written over the solved spectrum.
+//   F = 2 (green-jacobi): rows r^ (comps 0..d-1) and s^ (d..2d-1); q0 = r^H Gt r^,
+//                         q1 = s^H G s^; z^ replaces s^.
+//   F = 1 (green):        rows r^; q0 = r^H Gt r^, q1 = r^H G r^; z^ replaces r^.
+//   APPLY (F = 1):        rows of the input spectrum; z^ replaces it.
+// ---------------------------------------------------------------------------
+template <int D>
+struct HB {
+  double dg[D];
+  double re[3], im[3];
+};
+template <int D>
+__device__ __forceinline__ HB<D> ld_block(const double* __restrict__ b, int64_t Nh, int64_t f) {
+  HB<D> B;
+#pragma unroll
+  for (int a = 0; a < D; ++a) B.dg[a] = __ldg(b + a * Nh + f);
+  constexpr int NO = D == 2 ? 1 : 3;
+#pragma unroll
+  for (int k = 0; k < NO; ++k) {
+    B.re[k] = __ldg(b + (D + 2 * k) * Nh + f);
+    B.im[k] = __ldg(b + (D + 2 * k + 1) * Nh + f);
+  }
+  return B;
+}
+template <int D>
+__device__ __forceinline__ double hb_apply(const HB<D>& B, const double2 (&s)[D], double2 (&z)[D]) {
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double zr = B.dg[a] * s[a].x, zi = B.dg[a] * s[a].y;
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      if (b == a) continue;
+      const int lo = a < b ? a : b, hi = a < b ? b : a;
+      const int k = lo == 0 ? hi - 1 : 2;
+      const double gr = B.re[k];
+      const double gi = a < b ? B.im[k] : -B.im[k];
+      zr += gr * s[b].x - gi * s[b].y;
+      zi += gr * s[b].y + gi * s[b].x;
+    }
+    z[a] = make_double2(zr, zi);
+  }
+  double q = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) q += s[a].x * z[a].x + s[a].y * z[a].y;
+  return q;
+}
+
+// Several small CTAs per SM (two radix-8 butterflies per thread per stage, row
+// buffers only -- the Green planes stream straight from global): while one CTA
+// sits at an FFT-stage barrier or waits for its next rows, the others issue.
+constexpr int CPAD = 8;  // one padding slot every 8 elements of a row
+constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / 16); }
+constexpr int passC_bufd(int D, int L, int F) { return F * D * padded_len<CPAD>(L) * 2; }
+// resident CTAs per SM the launch bounds aim for (capped by shared memory)
+constexpr int passC_minb(int D, int L, int F) {
+  return passC_bufd(D, L, F) * 8 <= 72 * 1024 ? 3 : (passC_bufd(D, L, F) * 8 <= 110 * 1024 ? 2 : 1);
+}
+constexpr bool passC_db(int D, int L, int F) { return false; }
+
+template <int D, int L, int F, int MODE>
+__global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
+    passC(FGeom g, const PcgState* __restrict__ st, const double* __restrict__ gpc,
+          const double* __restrict__ gterm, double2* __restrict__ spec,
+          double* __restrict__ partials, const double2* __restrict__ tw) {
+  constexpr int NQ = F * D;  // rows held per frequency row
+  constexpr int NT = passC_nt(D, L, F);
+  constexpr int RL = padded_len<CPAD>(L);
+  constexpr int GP = 0;                               // Green planes are not staged
+  constexpr int BUFD = passC_bufd(D, L, F);           // doubles per stage buffer
+  constexpr bool DB = passC_db(D, L, F);
+  static_assert(BUFD == NQ * RL * 2 + GP * L, "buffer layout");
+  // [buf][ rows: NQ x RL double2 | Green planes: GP x L double ]
+  extern __shared__ double2 sbuf_all[];
+  __shared__ double red[64];
+  if (MODE != FM_APPLY && st->done) return;
+  static_assert(MODE != FM_QUAD || F == 1, "quad-only pass holds one spectrum");
+  const double invN = 1.0 / (double)g.N;
+  const int64_t rows = g.CS / L;
+  const int64_t Nh = g.CS;
+  double q0 = 0.0, q1 = 0.0;
+  constexpr int ZQ = F == 2 ? D : 0;  // first row of the solved spectrum
+  auto rows_of = [&](int b) { return sbuf_all + (size_t)b * (BUFD / 2); };
+  auto gbl_of = [&](int b) { return reinterpret_cast<double*>(rows_of(b) + NQ * RL); };
+  // stage row `row` (spectra + Green planes) into buffer b with cp.async
+  auto prefetch = [&](int64_t row, int b) {
+    double2* sb = rows_of(b);
+    double* gb = gbl_of(b);
+    const int64_t rbase = row * L;
+    for (int e = threadIdx.x; e < NQ * L; e += NT) {
+      const int q = e / L, k = e % L;
+      cpa16(sb + q * RL + pidx<CPAD>(k), spec + q * g.CS + rbase + k);
+    }
+    for (int e = threadIdx.x; e < GP * L; e += NT) {
+      const int p = e / L, k = e % L;
+      cpa8(gb + e, gpc + p * Nh + rbase + k);
+    }
+    cpa_commit();
+  };
+  int64_t row = blockIdx.x;
+  if (row < rows) prefetch(row, 0);
+  for (int it = 0; row < rows; ++it, row += gridDim.x) {
+    const int b = DB ? (it & 1) : 0;
+    if (DB) {
+      if (row + gridDim.x < rows) prefetch(row + gridDim.x, b ^ 1);
+      else cpa_commit();
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    double2* sbuf = rows_of(b);
+    const double* gsm = gbl_of(b);
+    const int64_t rbase = row * L;
+    const int k0 = (int)row / (int)(g.PS / L);
+    const double w = (k0 == 0 || 2 * k0 == g.n0) ? 1.0 : 2.0;
+    cta_fft<L, NQ, NT, false, false, CPAD>(sbuf, 1, RL, tw);
+#pragma unroll 1
+    for (int k = threadIdx.x; k < L; k += NT) {
+      const int64_t f = rbase + k;
+      const HB<D> B = ld_block<D>(gpc, Nh, f);
+      (void)gsm;
+      double2 s[D], z[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) s[a] = sbuf[(ZQ + a) * RL + pidx<CPAD>(k)];
+      const double qs = hb_apply<D>(B, s, z);
+      if (MODE == FM_QUAD) {
+        q0 += w * qs;  // gpc is the termination operator here
+      } else if (MODE != FM_APPLY) {
+        if (F == 2) {
+          double2 rr[D], tmp[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) rr[a] = sbuf[a * RL + pidx<CPAD>(k)];
+          const double qr = (gterm == gpc) ? hb_apply<D>(B, rr, tmp)
+                                           : hb_apply<D>(ld_block<D>(gterm, Nh, f), rr, tmp);
+          q0 += w * qr;
+          q1 += w * qs;
+        } else {
+          q1 += w * qs;
+          if (gterm == gpc) {
+            q0 += w * qs;
+          } else {
+            double2 tmp[D];
+            q0 += w * hb_apply<D>(ld_block<D>(gterm, Nh, f), s, tmp);
+          }
+        }
+      }
+#pragma unroll
+      if (MODE != FM_QUAD)
+#pragma unroll
+        for (int a = 0; a < D; ++a) sbuf[(ZQ + a) * RL + pidx<CPAD>(k)] = cscale(z[a], invN);
+    }
+    __syncthreads();
+    if (MODE != FM_QUAD) {
+      cta_fft<L, D, NT, true, false, CPAD>(sbuf + ZQ * RL, 1, RL, tw);
+      for (int e = threadIdx.x; e < D * L; e += NT) {
+        const int q = e / L, k = e % L;
+        spec[(ZQ + q) * g.CS + rbase + k] = sbuf[(ZQ + q) * RL + pidx<CPAD>(k)];
+      }
+      __syncthreads();
+    }
+    if (!DB && row + gridDim.x < rows) prefetch(row + gridDim.x, 0);
+  }
+  cpa_wait<0>();
+  if (MODE != FM_APPLY) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    q0 = warp_sum(q0 * invN);
+    q1 = warp_sum(q1 * invN);
+    if (lane == 0) { red[wid] = q0; red[32 + wid] = q1; }
+    __syncthreads();
+    if (wid == 0) {
+      double a = lane < NT / 32 ? red[lane] : 0.0, b = lane < NT / 32 ? red[32 + lane] : 0.0;
+      a = warp_sum(a);
+      b = warp_sum(b);
+      if (lane == 0) {
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pass I: axis-0 complex-to-real of z^ fused with the PCG direction update.
+//   FM_ITER:  if alpha is valid: x += alpha p ; unless done: p = Dz + beta p
+//   FM_INIT:  p = Dz
+//   FM_APPLY: out = Dz           (D = D^-1/2 for green-jacobi, identity for green)
+// ---------------------------------------------------------------------------
+constexpr int passI_nt(int M) { return nt_for(tw_a(M) * M / 4); }
+
+template <int M, int MODE>
+__global__ void __launch_bounds__(passI_nt(M))
+    passI(FGeom g, const PcgState* __restrict__ st, const double2* __restrict__ zspec,
+          const double* __restrict__ dinv, double* __restrict__ p, double* __restrict__ x,
+          double* __restrict__ out, const double2* __restrict__ tw) {
+  constexpr int TW = tw_a(M);
+  constexpr int NT = passI_nt(M);
+  extern __shared__ double2 sbuf[];  // [k][col], k <= M
+  if (MODE == FM_ITER && !st->xupd) return;
+  if (MODE == FM_INIT && st->done) return;
+  const int c = blockIdx.y;
+  const int64_t col0 = (int64_t)blockIdx.x * TW;
+  const double2* zc = zspec + c * g.CS + col0;
+  for (int e = threadIdx.x; e < (M + 1) * TW; e += NT) {
+    const int k = e / TW, col = e % TW;
+    cpa16(sbuf + e, zc + (int64_t)k * g.PS + col);
+  }
+  cpa_commit();
+  // the epilogue's D, p, x are fetched now, in flight during the transform
+  constexpr int PE = M * TW / NT;
+  static_assert(PE * NT == M * TW, "pass I tiling");
+  const bool use_d = dinv != nullptr;
+  double dv[PE][2], pv[PE][2], xv[PE][2];
+#pragma unroll
+  for (int j = 0; j < PE; ++j) {
+    const int e = threadIdx.x + j * NT;
+    const int m = e / TW, col = e % TW;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t idx = c * g.N + (int64_t)(2 * m + h) * g.PS + col0 + col;
+      dv[j][h] = use_d ? __ldg(dinv + idx) : 1.0;
+      if (MODE == FM_ITER) { pv[j][h] = p[idx]; xv[j][h] = x[idx]; }
+    }
+  }
+  cpa_wait<0>();
+  __syncthreads();
+  // Z'[k] = (X[k] + conj X[M-k]) + i e^{+2 pi i k / n0} (X[k] - conj X[M-k]),
+  // computed pairwise (k, M-k) in place; k = 0 pairs with the Nyquist row M
+  constexpr int TWS = kTwN / (2 * M);
+  for (int e = threadIdx.x; e < (M / 2 + 1) * TW; e += NT) {
+    const int k = e / TW, col = e % TW;
+    const int kc = M - k;
+    const double2 xa = sbuf[k * TW + col], xb = sbuf[kc * TW + col];
+    const double2 wa = cconj(__ldg(tw + ((k * TWS) & (kTwN - 1))));
+    const double2 wb = cconj(__ldg(tw + ((kc * TWS) & (kTwN - 1))));
+    const double2 za = cadd(cadd(xa, cconj(xb)), mul_mi<true>(cmul(wa, csub(xa, cconj(xb)))));
+    const double2 zb = cadd(cadd(xb, cconj(xa)), mul_mi<true>(cmul(wb, csub(xb, cconj(xa)))));
+    sbuf[k * TW + col] = za;
+    if (kc != M && kc != k) sbuf[kc * TW + col] = zb;
+  }
+  __syncthreads();
+  cta_fft<M, TW, NT, true>(sbuf, TW, 1, tw);
+  const bool done = MODE == FM_ITER ? (st->done != 0) : false;
+  const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
+  const double beta = MODE == FM_ITER ? st->beta : 0.0;
+#pragma unroll
+  for (int j = 0; j < PE; ++j) {
+    const int e = threadIdx.x + j * NT;
+    const int m = e / TW, col = e % TW;
+    const double2 z = sbuf[e];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t idx = c * g.N + (int64_t)(2 * m + h) * g.PS + col0 + col;
+      double zz = h ? z.y : z.x;
+      if (use_d) zz = dv[j][h] * zz;
+      if (MODE == FM_APPLY) {
+        out[idx] = zz;
+      } else if (MODE == FM_INIT) {
+        p[idx] = zz;
+      } else {
+        const double pold = pv[j][h];
+        x[idx] = xv[j][h] + alpha * pold;
+        if (!done) p[idx] = beta * pold + zz;
+      }
+    }
+  }
+}
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    JF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+FGeom fgeom(const Geom& g) {
+  FGeom f{};
+  f.d = g.d;
+  f.n0 = g.n[0];
+  f.nlast = g.n[g.d - 1];
+  f.M0 = g.n[0] / 2;
+  f.K0 = f.M0 + 1;
+  f.N = g.N;
+  f.PS = g.N / g.n[0];
+  f.CS = (int64_t)f.K0 * f.PS;
+  f.n1 = g.d == 3 ? g.n[1] : 1;
+  return f;
+}
+
+// ---- size dispatch -------------------------------------------------------
+template <int M, int F, int MODE>
+void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, const double* kp,
+               const double* dinv, double2* spec, const double2* tw) {
+  constexpr int TW = tw_a(M);
+  constexpr int NT = nt_for(F * TW * M / 8);
+  // raw staging (3 arrays x 2M x TW doubles) aliases the packed tile
+  const size_t smem = std::max(sizeof(double2) * F * TW * M, sizeof(double) * 3 * 2 * M * TW);
+  auto k = passA<M, F, MODE>;
+  static bool attr = false;
+  if (!attr) { set_smem(k, smem); attr = true; }
+  dim3 grid((unsigned)(g.PS / TW), g.d);
+  k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
+  JF_LAUNCHED();
+}
+template <int L, bool INV, bool PRED>
+void launchB_L(const FGeom& g, cudaStream_t s, const PcgState* st, double2* spec, int comp0,
+               int ncomp, const double2* tw) {
+  constexpr int TW = tw_b(L);
+  constexpr int NT = nt_for(TW * L / 8);
+  const size_t smem = sizeof(double2) * TW * L;
+  auto k = passB<L, INV, PRED>;
+  static bool attr = false;
+  if (!attr) { set_smem(k, smem); attr = true; }
+  dim3 grid((unsigned)(g.nlast / TW), g.K0, ncomp);
+  k<<<grid, NT, smem, s>>>(g, st, spec, comp0, g.nlast, tw);
+  JF_LAUNCHED();
+}
+template <int D, int L, int F, int MODE>
+int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* gpc,
+              const double* gterm, double2* spec, double* partials, const double2* tw) {
+  constexpr int NT = passC_nt(D, L, F);
+  constexpr int BUFD = passC_bufd(D, L, F);
+  constexpr bool DB = passC_db(D, L, F);
+  const size_t smem = sizeof(double) * BUFD * (DB ? 2 : 1);
+  auto k = passC<D, L, F, MODE>;
+  static int per_sm = -1;  // per instantiation
+  if (per_sm < 0) {
+    set_smem(k, smem);
+    JF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, smem));
+  }
+  const int64_t rows = g.CS / L;
+  const int blocks = (int)std::min<int64_t>(rows, (int64_t)std::max(per_sm, 1) * 148 * 4);
+  k<<<blocks, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw);
+  JF_LAUNCHED();
+  return blocks;
+}
+template <int M, int MODE>
+void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2* zspec,
+               const double* dinv, double* p, double* x, double* out, const double2* tw) {
+  constexpr int TW = tw_a(M);
+  constexpr int NT = passI_nt(M);
+  const size_t smem = sizeof(double2) * TW * (M + 1);
+  auto k = passI<M, MODE>;
+  static bool attr = false;
+  if (!attr) { set_smem(k, smem); attr = true; }
+  dim3 grid((unsigned)(g.PS / TW), g.d);
+  k<<<grid, NT, smem, s>>>(g, st, zspec, dinv, p, x, out, tw);
+  JF_LAUNCHED();
+}
+
+#define JF_SIZE_SWITCH(L, CALL)                   \
+  switch (L) {                                    \
+    case 16: { constexpr int LL = 16; CALL; break; }   \
+    case 32: { constexpr int LL = 32; CALL; break; }   \
+    case 64: { constexpr int LL = 64; CALL; break; }   \
+    case 128: { constexpr int LL = 128; CALL; break; } \
+    case 256: { constexpr int LL = 256; CALL; break; } \
+    case 512: { constexpr int LL = 512; CALL; break; } \
+    case 1024: { constexpr int LL = 1024; CALL; break; } \
+    case 2048: { constexpr int LL = 2048; CALL; break; } \
+    default: throw Error(JFFTB_EINVAL, "fused FFT: unsupported size"); \
+  }
+
+void launchA(const FGeom& g, cudaStream_t s, int F, int mode, const PcgState* st, double* r,
+             const double* kp, const double* dinv, double2* spec, const double2* tw) {
+  const int n0 = g.n0;
+  if (F == 2) {
+    if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 2, FM_ITER>(g, s, st, r, kp, dinv, spec, tw))); }
+    else { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 2, FM_INIT>(g, s, st, r, kp, dinv, spec, tw))); }
+  } else {
+    if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_ITER>(g, s, st, r, kp, dinv, spec, tw))); }
+    else if (mode == FM_INIT) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_INIT>(g, s, st, r, kp, dinv, spec, tw))); }
+    else { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_APPLY>(g, s, st, r, kp, dinv, spec, tw))); }
+  }
+}
+void launchB(const FGeom& g, cudaStream_t s, bool inv, bool pred, const PcgState* st,
+             double2* spec, int comp0, int ncomp, const double2* tw) {
+  const int n1 = g.n1;
+  if (inv) {
+    if (pred) { JF_SIZE_SWITCH(n1, (launchB_L<LL, true, true>(g, s, st, spec, comp0, ncomp, tw))); }
+    else { JF_SIZE_SWITCH(n1, (launchB_L<LL, true, false>(g, s, st, spec, comp0, ncomp, tw))); }
+  } else {
+    if (pred) { JF_SIZE_SWITCH(n1, (launchB_L<LL, false, true>(g, s, st, spec, comp0, ncomp, tw))); }
+    else { JF_SIZE_SWITCH(n1, (launchB_L<LL, false, false>(g, s, st, spec, comp0, ncomp, tw))); }
+  }
+}
+int launchC(const FGeom& g, cudaStream_t s, int F, int mode, const PcgState* st,
+            const double* gpc, const double* gterm, double2* spec, double* partials,
+            const double2* tw) {
+  const int nl = g.nlast;
+  int blocks = 0;
+  if (g.d == 3) {
+    if (mode == FM_APPLY) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 1, FM_APPLY>(g, s, st, gpc, gterm, spec, partials, tw))); }
+    else if (F == 2) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 2, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw))); }
+    else { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 1, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw))); }
+  } else {
+    if (mode == FM_APPLY) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 1, FM_APPLY>(g, s, st, gpc, gterm, spec, partials, tw))); }
+    else if (F == 2) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 2, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw))); }
+    else { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 1, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw))); }
+  }
+  return blocks;
+}
+void launchI(const FGeom& g, cudaStream_t s, int mode, const PcgState* st, const double2* zspec,
+             const double* dinv, double* p, double* x, double* out, const double2* tw) {
+  const int n0 = g.n0;
+  if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchI_M<LL / 2, FM_ITER>(g, s, st, zspec, dinv, p, x, out, tw))); }
+  else if (mode == FM_INIT) { JF_SIZE_SWITCH(n0, (launchI_M<LL / 2, FM_INIT>(g, s, st, zspec, dinv, p, x, out, tw))); }
+  else { JF_SIZE_SWITCH(n0, (launchI_M<LL / 2, FM_APPLY>(g, s, st, zspec, dinv, p, x, out, tw))); }
+}
+
+}  // namespace
+
+void launch_twiddles(cudaStream_t s, double2* tw) {
+  twiddle_kernel<<<kTwN / 256, 256, 0, s>>>(tw);
+  JF_LAUNCHED();
+}
+
+bool fused_supported(const Geom& g) {
+  for (int a = 0; a < g.d; ++a) {
+    const int n = g.n[a];
+    if (n < 16 || n > 2048 || (n & (n - 1))) return false;
+  }
+  return true;
+}
+
+int64_t fused_spec_elems(const Geom& g) { return (int64_t)(g.n[0] / 2 + 1) * (g.N / g.n[0]); }
+
+// apply the Green (dinv == null) or Green-Jacobi preconditioner through the
+// fused passes: out = D G D r  (spec: d * CS complex scratch)
+void fused_precond_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
+                         const double* dinv, const double* r, double* out, double2* spec,
+                         const double2* tw) {
+  const FGeom g = fgeom(geo);
+  launchA(g, s, 1, FM_APPLY, nullptr, const_cast<double*>(r), nullptr, dinv, spec, tw);
+  if (g.d == 3) launchB(g, s, false, false, nullptr, spec, 0, g.d, tw);
+  launchC(g, s, 1, FM_APPLY, nullptr, gblocks, gblocks, spec, nullptr, tw);
+  if (g.d == 3) launchB(g, s, true, false, nullptr, spec, 0, g.d, tw);
+  launchI(g, s, FM_APPLY, nullptr, spec, dinv, nullptr, nullptr, out, tw);
+}
+
+// ---- the PCG stages (pcg.cu strings them together) ------------------------
+// A: mode FUSED_INIT / FUSED_ITER with F = 1 (green) or 2 (green-jacobi);
+//    FUSED_APPLY transforms r (dinv == null) for the quad-only termination
+void fused_stage_A(const Geom& geo, cudaStream_t s, int F, int mode, const PcgState* st,
+                   double* r, const double* kp, const double* dinv, double2* spec,
+                   const double2* tw) {
+  launchA(fgeom(geo), s, F, mode, st, r, kp, dinv, spec, tw);
+}
+void fused_stage_B(const Geom& geo, cudaStream_t s, bool inv, const PcgState* st,
+                   double2* spec, int ncomp, const double2* tw) {
+  const FGeom g = fgeom(geo);
+  if (g.d == 3) launchB(g, s, inv, true, st, spec, 0, ncomp, tw);
+}
+// returns the number of partial pairs written
+int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const PcgState* st,
+                  const double* gpc, const double* gterm, double2* spec, double* partials,
+                  const double2* tw) {
+  const FGeom g = fgeom(geo);
+  if (quad_only) {
+    int blocks = 0;
+    if (g.d == 3) {
+      JF_SIZE_SWITCH(g.nlast, (blocks = launchC_L<3, LL, 1, FM_QUAD>(g, s, st, gpc, gterm, spec, partials, tw)));
+    } else {
+      JF_SIZE_SWITCH(g.nlast, (blocks = launchC_L<2, LL, 1, FM_QUAD>(g, s, st, gpc, gterm, spec, partials, tw)));
+    }
+    return blocks;
+  }
+  return launchC(g, s, F, FM_ITER, st, gpc, gterm, spec, partials, tw);
+}
+void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
+                   const double2* zspec, const double* dinv, double* p, double* x,
+                   const double2* tw) {
+  launchI(fgeom(geo), s, mode, st, zspec, dinv, p, x, nullptr, tw);
+}
+int64_t fused_component_stride(const Geom& geo) { return fgeom(geo).CS; }
+
+}  // namespace jfftb

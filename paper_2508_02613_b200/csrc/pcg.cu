@@ -44,10 +44,14 @@ __device__ double sum_strided(const double* p, int count, int stride, int j, dou
 
 __global__ void alpha_kernel(PcgState* st, const double* __restrict__ partials, int count) {
   __shared__ double red[32];
-  if (st->done) return;
+  if (st->done) {
+    if (threadIdx.x == 0) st->xupd = 0;
+    return;
+  }
   const double curv = sum_strided(partials, count, 1, 0, red);
   if (threadIdx.x == 0) {
     st->curv = curv;
+    st->xupd = 0;
     if (!isfinite(curv)) {
       st->status = JFFTB_ENONFINITE;
       st->done = 1;
@@ -56,6 +60,7 @@ __global__ void alpha_kernel(PcgState* st, const double* __restrict__ partials, 
       st->done = 1;
     } else {
       st->alpha = st->rz / curv;
+      st->xupd = 1;
     }
   }
 }
@@ -206,6 +211,63 @@ static void pcg_precond_phase(jfftb_grid* g, jfftb_jacobi* jac, jfftb_green* gpc
   }
 }
 
+// Fused-spectral variant (power-of-two grids): green / green-jacobi run the
+// five fused passes of fused.cu, the x update rides on the last one (pass I);
+// none / jacobi keep their elementwise update and get the termination
+// functional from a quad-only spectral pass.
+template <int KIND, bool INIT>
+static void pcg_precond_phase_fused(jfftb_grid* g, jfftb_jacobi* jac, jfftb_green* gpc,
+                                    jfftb_green* gterm, const PcgBuffers& B) {
+  const Geom& geo = g->geo;
+  const int64_t n = geo.d * geo.N;
+  cudaStream_t s = g->stream;
+  const double* dinv = jac ? jac->inv_sqrt : nullptr;
+  const double2* tw = g->twiddle;
+  double* r = B.rs;
+  double* sz = B.rs + n;
+  constexpr bool GJ = KIND == JFFTB_PC_GREEN_JACOBI;
+  constexpr bool SPECTRAL_PC = GJ || KIND == JFFTB_PC_GREEN;
+  constexpr int F = GJ ? 2 : 1;
+  int scount;
+  if (SPECTRAL_PC) {
+    fused_stage_A(geo, s, F, INIT ? FUSED_INIT : FUSED_ITER, B.st, r, B.kp, dinv, B.spec, tw);
+    if (!INIT) prof_mark(g);
+    fused_stage_B(geo, s, false, B.st, B.spec, F * geo.d, tw);
+    if (!INIT) prof_mark(g);
+    scount = fused_stage_C(geo, s, F, false, B.st, gpc->blocks, gterm->blocks, B.spec, B.spart, tw);
+  } else {
+    update_kernel<KIND, INIT><<<kRedBlocks, 256, 0, s>>>(n, B.st, B.x, r, B.p, B.kp, dinv, sz,
+                                                         B.upart);
+    JF_LAUNCHED();
+    if (!INIT) prof_mark(g);
+    fused_stage_A(geo, s, 1, FUSED_APPLY, B.st, r, nullptr, nullptr, B.spec, tw);
+    fused_stage_B(geo, s, false, B.st, B.spec, geo.d, tw);
+    if (!INIT) prof_mark(g);
+    scount = fused_stage_C(geo, s, 1, true, B.st, gterm->blocks, gterm->blocks, B.spec, B.spart, tw);
+  }
+  if (!INIT) prof_mark(g);
+  finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, scount, B.upart, kRedBlocks,
+                                                 B.hist);
+  JF_LAUNCHED();
+  if (!INIT) prof_mark(g);
+  if (SPECTRAL_PC) {
+    double2* z = B.spec + (GJ ? geo.d * fused_component_stride(geo) : 0);
+    fused_stage_B(geo, s, true, B.st, z, geo.d, tw);
+    if (!INIT) prof_mark(g);
+    fused_stage_I(geo, s, INIT ? FUSED_INIT : FUSED_ITER, B.st, z, GJ ? dinv : nullptr, B.p, B.x,
+                  tw);
+  } else {
+    if (!INIT) prof_mark(g);
+    pupdate_kernel<KIND, INIT><<<grid_n(n), 256, 0, s>>>(n, B.st, B.p,
+                                                         KIND == JFFTB_PC_JACOBI ? sz : r, dinv);
+    JF_LAUNCHED();
+  }
+  if (!INIT) {
+    prof_mark(g);
+    prof_end_iter(g);
+  }
+}
+
 template <int KIND>
 static void pcg_iteration(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
                           jfftb_green* gterm, const PcgBuffers& B) {
@@ -217,13 +279,15 @@ static void pcg_iteration(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
   alpha_kernel<<<1, 1024, 0, s>>>(B.st, B.kpart, B.kcount);
   JF_LAUNCHED();
   prof_mark(g);
-  pcg_precond_phase<KIND, false>(g, jac, gpc, gterm, B);
+  if (g->fused) pcg_precond_phase_fused<KIND, false>(g, jac, gpc, gterm, B);
+  else pcg_precond_phase<KIND, false>(g, jac, gpc, gterm, B);
 }
 
 template <int KIND>
 static void pcg_init(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc, jfftb_green* gterm,
                      const PcgBuffers& B) {
-  pcg_precond_phase<KIND, true>(op->grid, jac, gpc, gterm, B);
+  if (op->grid->fused) pcg_precond_phase_fused<KIND, true>(op->grid, jac, gpc, gterm, B);
+  else pcg_precond_phase<KIND, true>(op->grid, jac, gpc, gterm, B);
 }
 
 void pcg_dispatch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,

@@ -210,20 +210,28 @@ __device__ void herm_pinv(const double (&Hr)[D][D], const double (&Hi)[D][D],
     }
 }
 
+// layout 0: numpy rfftn half spectrum (last axis halved), nfreq = Nh;
+// layout 1: fused.cu half spectrum (axis 0 halved), nfreq = (n0/2+1) N / n0
 template <int D>
 __global__ void green_setup_kernel(Geom g, const double* __restrict__ resp, int m0, int m1,
-                                   int m2, double* __restrict__ blocks) {
+                                   int m2, double* __restrict__ blocks, int layout,
+                                   int64_t nfreq) {
   // resp: D impulse responses (beta) of D components on the small m-grid
   const int m[3] = {m0, m1, m2};
   int64_t msz = 1;
   for (int a = 0; a < D; ++a) msz *= m[a];
-  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < g.Nh;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nfreq;
        f += (int64_t)gridDim.x * blockDim.x) {
     int q[3];
     int64_t rem = f;
-    q[D - 1] = (int)(rem % g.nh);
-    rem /= g.nh;
-    for (int a = D - 2; a >= 0; --a) { q[a] = (int)(rem % g.n[a]); rem /= g.n[a]; }
+    if (layout == 0) {
+      q[D - 1] = (int)(rem % g.nh);
+      rem /= g.nh;
+      for (int a = D - 2; a >= 0; --a) { q[a] = (int)(rem % g.n[a]); rem /= g.n[a]; }
+    } else {
+      for (int a = D - 1; a >= 1; --a) { q[a] = (int)(rem % g.n[a]); rem /= g.n[a]; }
+      q[0] = (int)rem;
+    }
     double Kr[D][D], Ki[D][D];
 #pragma unroll
     for (int a = 0; a < D; ++a)
@@ -276,14 +284,14 @@ __global__ void green_setup_kernel(Geom g, const double* __restrict__ resp, int 
         for (int b = 0; b < D; ++b) Pr[a][b] = Pi[a][b] = 0.0;
     }
 #pragma unroll
-    for (int a = 0; a < D; ++a) blocks[a * g.Nh + f] = Pr[a][a];
+    for (int a = 0; a < D; ++a) blocks[a * nfreq + f] = Pr[a][a];
     int k = 0;
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
       for (int b = a + 1; b < D; ++b) {
-        blocks[(D + 2 * k) * g.Nh + f] = 0.5 * (Pr[a][b] + Pr[b][a]);
-        blocks[(D + 2 * k + 1) * g.Nh + f] = 0.5 * (Pi[a][b] - Pi[b][a]);
+        blocks[(D + 2 * k) * nfreq + f] = 0.5 * (Pr[a][b] + Pr[b][a]);
+        blocks[(D + 2 * k + 1) * nfreq + f] = 0.5 * (Pi[a][b] - Pi[b][a]);
         ++k;
       }
   }
@@ -306,13 +314,16 @@ void launch_green_apply(const Geom& g, cudaStream_t s, const double* blocks, con
   }
 }
 
-void launch_green_setup(const Geom& g, cudaStream_t s, const double* resp, int m3, double* blocks) {
+void launch_green_setup(const Geom& g, cudaStream_t s, const double* resp, int m3, double* blocks,
+                        int layout, int64_t nfreq) {
   // m3 packs the small-grid extents as m0 | m1 << 8 | m2 << 16
   const int m0 = m3 & 0xff, m1 = (m3 >> 8) & 0xff, m2 = (m3 >> 16) & 0xff;
   if (g.d == 3)
-    green_setup_kernel<3><<<spec_blocks(g.Nh), 128, 0, s>>>(g, resp, m0, m1, m2, blocks);
+    green_setup_kernel<3><<<spec_blocks(nfreq), 128, 0, s>>>(g, resp, m0, m1, m2, blocks, layout,
+                                                             nfreq);
   else
-    green_setup_kernel<2><<<spec_blocks(g.Nh), 128, 0, s>>>(g, resp, m0, m1, m2, blocks);
+    green_setup_kernel<2><<<spec_blocks(nfreq), 128, 0, s>>>(g, resp, m0, m1, m2, blocks, layout,
+                                                             nfreq);
   JF_LAUNCHED();
 }
 

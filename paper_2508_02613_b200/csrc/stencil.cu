@@ -70,15 +70,40 @@ __host__ EbarT make_ebar(int d, const double* m) {
 // --------------------------------------------------------------------------
 // 3-D plane-march stencil
 // --------------------------------------------------------------------------
+// One warp per tile row (BX3 = 32 lanes along the contiguous axis 2).  Per
+// layer the displacement plane two layers ahead and the density layer one
+// ahead stream global -> shared with cp.async (no registers held, latency
+// hidden behind a whole layer of voxel math) into 3-deep rings; corner
+// displacements are read from the ring, forces for the +x neighbour travel by
+// warp shuffle and the combined +y forces through a double-buffered smem row.
+// One __syncthreads per layer.
+constexpr int S3_U = 3 * 3 * (BY3 + 1) * (BX3 + 1);  // u ring: [slot][comp][y][x]
+constexpr int S3_R = 3 * BY3 * BX3;                  // rho ring: [slot][y][x]
+constexpr int S3_F = 2 * 2 * 3 * BY3 * BX3;          // +y hand-over: [buf][plane][comp][y][x]
+constexpr size_t S3_BYTES = sizeof(double) * (S3_U + S3_R + S3_F + 32);
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 template <int MODE, bool SCALE>
-__global__ void __launch_bounds__(BX3* BY3)
+__global__ void __launch_bounds__(BX3* BY3, 2)
     stencil3d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
               double lam0, double mu0, EbarT E, double* __restrict__ out,
               double* __restrict__ partials, int chunk) {
   constexpr bool HAS_U = MODE != VOX_RHS;
-  __shared__ double U[3][BY3 + 1][BX3 + 1];
-  __shared__ double F[3][2][3][BY3][BX3];  // [dir x,y,xy][plane k,k+1][comp]
-  __shared__ double red[32];
+  extern __shared__ double smem[];
+  double(*U)[3][BY3 + 1][BX3 + 1] = reinterpret_cast<double(*)[3][BY3 + 1][BX3 + 1]>(smem);
+  double(*R)[BY3][BX3] = reinterpret_cast<double(*)[BY3][BX3]>(smem + S3_U);
+  double(*Fy)[2][3][BY3][BX3] =
+      reinterpret_cast<double(*)[2][3][BY3][BX3]>(smem + S3_U + S3_R);
+  double* red = smem + S3_U + S3_R + S3_F;
 
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const int64_t P = (int64_t)n1 * n2;
@@ -91,60 +116,71 @@ __global__ void __launch_bounds__(BX3* BY3)
   const bool outp = tx >= 1 && ty >= 1 && gx < n2 && gy < n1;
   const int c2h = wrapi(X0 - 1 + BX3, n2), c1h = wrapi(Y0 - 1 + BY3, n1);
   const int64_t col = (int64_t)c1 * n2 + c2;
+  const bool hx = tx == BX3 - 1, hy = ty == BY3 - 1;
+  const int64_t colx = (int64_t)c1 * n2 + c2h, coly = (int64_t)c1h * n2 + c2,
+                colxy = (int64_t)c1h * n2 + c2h;
 
   double gs[3], fs[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) { gs[a] = g.hinv[a]; fs[a] = g.hinv[a]; }
   const double (*Eb)[3] = E.e;
 
-  auto load_plane = [&](int k) {
+  // async fetch of layer kk (unwrapped, kk >= -1) into ring slot (kk+3)%3
+  auto fetch_u = [&](int kk) {
     if (!HAS_U) return;
-    const int64_t base = (int64_t)k * P;
+    const int s = (kk + 3) % 3;
+    const double* ub = u + (int64_t)wrapi(kk, n0) * P;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const double* ui = u + i * g.N + base;
-      U[i][ty][tx] = __ldg(ui + col);
-      if (tx == BX3 - 1) U[i][ty][BX3] = __ldg(ui + (int64_t)c1 * n2 + c2h);
-      if (ty == BY3 - 1) U[i][BY3][tx] = __ldg(ui + (int64_t)c1h * n2 + c2);
-      if (tx == BX3 - 1 && ty == BY3 - 1) U[i][BY3][BX3] = __ldg(ui + (int64_t)c1h * n2 + c2h);
+      const double* ui = ub + i * g.N;
+      cp_async8(&U[s][i][ty][tx], ui + col);
+      if (hx) cp_async8(&U[s][i][ty][BX3], ui + colx);
+      if (hy) cp_async8(&U[s][i][BY3][tx], ui + coly);
+      if (hx && hy) cp_async8(&U[s][i][BY3][BX3], ui + colxy);
     }
   };
-  auto read_corners = [&](double (&q)[4][3]) {
+  auto fetch_r = [&](int kk) {
+    if (rho) cp_async8(&R[(kk + 3) % 3][ty][tx], rho + (int64_t)wrapi(kk, n0) * P + col);
+  };
+  auto read_corners = [&](int kk, double (&q)[4][3]) {
+    const int s = (kk + 3) % 3;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      q[0][i] = U[i][ty][tx];
-      q[1][i] = U[i][ty][tx + 1];
-      q[2][i] = U[i][ty + 1][tx];
-      q[3][i] = U[i][ty + 1][tx + 1];
+      q[0][i] = U[s][i][ty][tx];
+      q[1][i] = U[s][i][ty][tx + 1];
+      q[2][i] = U[s][i][ty + 1][tx];
+      q[3][i] = U[s][i][ty + 1][tx + 1];
     }
   };
 
   double uk[4][3], uk1[4][3];
-  const int kstart = wrapi(k0 - 1, n0);
-  if (HAS_U) {
-    load_plane(kstart);
-    __syncthreads();
-    read_corners(uk);
-    __syncthreads();
-  } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int i = 0; i < 3; ++i) uk[q][i] = uk1[q][i] = 0.0;
-  }
+    for (int i = 0; i < 3; ++i) uk[q][i] = uk1[q][i] = 0.0;
+  // prologue: group A = planes k0-1, k0 and rho(k0-1); group B = plane k0+1, rho(k0)
+  fetch_u(k0 - 1);
+  fetch_u(k0);
+  fetch_r(k0 - 1);
+  cp_async_commit();
+  fetch_u(k0 + 1);
+  fetch_r(k0);
+  cp_async_commit();
+  cp_async_wait<1>();
+  __syncthreads();
+  if (HAS_U) read_corners(k0 - 1, uk);
 
   double nxt[3] = {0.0, 0.0, 0.0};
   double csum = 0.0;
-  for (int kk = k0 - 1; kk < k1; ++kk) {
-    const int k = wrapi(kk, n0);
-    const int kp = (k + 1 == n0) ? 0 : k + 1;
-    if (HAS_U) {
-      load_plane(kp);
-      __syncthreads();
-      read_corners(uk1);
-    }
-    const double r = rho ? __ldg(rho + (int64_t)k * P + col) : 1.0;
-    double lam = lam0 * r, mu = mu0 * r;
+  int64_t obase = (int64_t)wrapi(k0 - 1, n0) * P + col;  // output index of layer kk
+  for (int kk = k0 - 1, j = 0; kk < k1; ++kk, ++j) {
+    const int b = j & 1;
+    if (HAS_U) read_corners(kk + 1, uk1);
+    const double r = rho ? R[(kk + 3) % 3][ty][tx] : 1.0;
+    // refill: plane kk+3 takes plane kk's slot, rho(kk+2) takes rho(kk-1)'s
+    if (kk + 3 <= k1) fetch_u(kk + 3);
+    if (kk + 2 < k1) fetch_r(kk + 2);
+    cp_async_commit();
     double uc[8][3];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -153,42 +189,44 @@ __global__ void __launch_bounds__(BX3* BY3)
       for (int i = 0; i < 3; ++i) uc[c][i] = (c & 1) ? uk1[q][i] : uk[q][i];
     }
     double f[8][3];
-    voxel_forces<3, MODE, SCALE>(uc, lam, mu, gs, fs, Eb, f);
+    voxel_forces<3, MODE, SCALE>(uc, lam0 * r, mu0 * r, gs, fs, Eb, f);
     double ak[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      ak[i] = nxt[i] + f[0][i];
-      nxt[i] = f[1][i];
-      F[0][0][i][ty][tx] = f[4][i];
-      F[0][1][i][ty][tx] = f[5][i];
-      F[1][0][i][ty][tx] = f[2][i];
-      F[1][1][i][ty][tx] = f[3][i];
-      F[2][0][i][ty][tx] = f[6][i];
-      F[2][1][i][ty][tx] = f[7][i];
+      // +x neighbour (lane - 1) hands over its corners (0,0,1), (1,0,1); its
+      // (.,1,1) corners join our +y hand-over
+      const double x0 = __shfl_up_sync(0xffffffffu, f[4][i], 1);
+      const double x1 = __shfl_up_sync(0xffffffffu, f[5][i], 1);
+      const double y0 = __shfl_up_sync(0xffffffffu, f[6][i], 1);
+      const double y1 = __shfl_up_sync(0xffffffffu, f[7][i], 1);
+      ak[i] = nxt[i] + f[0][i] + x0;
+      nxt[i] = f[1][i] + x1;
+      Fy[b][0][i][ty][tx] = f[2][i] + (tx >= 1 ? y0 : 0.0);
+      Fy[b][1][i][ty][tx] = f[3][i] + (tx >= 1 ? y1 : 0.0);
     }
+    cp_async_wait<1>();  // plane kk+2 / rho(kk+1) landed (needed next layer)
     __syncthreads();
-    if (tx >= 1 && ty >= 1) {
+    if (ty >= 1) {
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        ak[i] = ak[i] + F[0][0][i][ty][tx - 1] + F[1][0][i][ty - 1][tx] +
-                F[2][0][i][ty - 1][tx - 1];
-        nxt[i] = nxt[i] + F[0][1][i][ty][tx - 1] + F[1][1][i][ty - 1][tx] +
-                 F[2][1][i][ty - 1][tx - 1];
+        ak[i] += Fy[b][0][i][ty - 1][tx];
+        nxt[i] += Fy[b][1][i][ty - 1][tx];
       }
     }
     if (kk >= k0 && outp) {
-      const int64_t idx = (int64_t)k * P + col;
 #pragma unroll
-      for (int i = 0; i < 3; ++i) out[i * g.N + idx] = ak[i];
+      for (int i = 0; i < 3; ++i) out[i * g.N + obase] = ak[i];
       if (MODE == VOX_K && partials)
         csum += uk[0][0] * ak[0] + uk[0][1] * ak[1] + uk[0][2] * ak[2];
     }
+    obase += P;
+    if (obase >= g.N) obase -= g.N;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int i = 0; i < 3; ++i) uk[q][i] = uk1[q][i];
-    if (!HAS_U) __syncthreads();  // F is rewritten next layer
   }
+  cp_async_wait<0>();
   if (MODE == VOX_K && partials) {
     const double s = block_sum(csum, red);
     if (threadIdx.x == 0 && threadIdx.y == 0)
@@ -300,9 +338,11 @@ StencilLaunch stencil_config(const Geom& g) {
   StencilLaunch L{};
   const int target = 4 * 148;
   if (g.d == 3) {
+    // ~16 waves of 2 resident CTAs per SM; marches of >= 16 layers so the
+    // per-chunk halo layer stays cheap
     const int bx = (g.n[2] + BX3 - 2) / (BX3 - 1), by = (g.n[1] + BY3 - 2) / (BY3 - 1);
-    int chunks = (target + bx * by - 1) / (bx * by);
-    chunks = std::max(1, std::min(chunks, g.n[0]));
+    int chunks = (16 * 2 * 148 + bx * by - 1) / (bx * by);
+    chunks = std::max(1, std::min(chunks, g.n[0] / 16));
     L.chunk = (g.n[0] + chunks - 1) / chunks;
     chunks = (g.n[0] + L.chunk - 1) / L.chunk;
     L.grid = dim3(bx, by, chunks);
@@ -323,9 +363,16 @@ template <int MODE, bool SCALE>
 void launch_mode(const Geom& g, cudaStream_t s, const StencilLaunch& L, const double* u,
                  const double* rho, double lam, double mu, const EbarT& E, double* out,
                  double* partials) {
-  if (g.d == 3)
-    stencil3d<MODE, SCALE><<<L.grid, L.block, 0, s>>>(g, u, rho, lam, mu, E, out, partials,
-                                                      L.chunk);
+  if (g.d == 3) {
+    static bool attr = false;  // per template instance
+    if (!attr) {
+      JF_CUDA(cudaFuncSetAttribute(stencil3d<MODE, SCALE>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S3_BYTES));
+      attr = true;
+    }
+    stencil3d<MODE, SCALE><<<L.grid, L.block, S3_BYTES, s>>>(g, u, rho, lam, mu, E, out,
+                                                             partials, L.chunk);
+  }
   else
     stencil2d<MODE, SCALE><<<L.grid, L.block, 0, s>>>(g, u, rho, lam, mu, E, out, partials,
                                                       L.chunk);
