@@ -152,6 +152,15 @@ int jfftb_profile_start(jfftb_grid* g);
  * (iterations that ran past convergence are not counted); stop != 0 disables */
 int jfftb_profile_read(jfftb_grid* g, double* stage_ms, int64_t* iterations, int stop);
 
+/* ---- diagnostics (tests only) ------------------------------------------ */
+/* Run the fused Green(-Jacobi) application up to pass `upto` (1 axis-0 R2C,
+ * 2 axis-1 FFT, 3 last-axis FFT + block solve + iFFT, 4 axis-1 iFFT,
+ * 5 axis-0 C2R) on host input r; out receives the intermediate spectrum
+ * (d x (n0/2+1) x n1 [x n2] complex) or, for upto = 5, the result.
+ * EINVAL on grids without the fused path (non power-of-two, n < 16). */
+int jfftb_debug_fused_apply(jfftb_green* green, jfftb_jacobi* jac, int upto, const double* r,
+                            double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,7 @@ _SIGS = {
                             _D, C.POINTER(C.c_int), C.POINTER(C.c_int), _D]),
     "jfftb_profile_start": (C.c_int, [_P]),
     "jfftb_profile_read": (C.c_int, [_P, _D, _I64, C.c_int]),
+    "jfftb_debug_fused_apply": (C.c_int, [_P, _P, C.c_int, _P, _P]),
 }
 EXPORTED = tuple(_SIGS)
 

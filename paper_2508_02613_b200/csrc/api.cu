@@ -886,6 +886,30 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
   });
 }
 
+int jfftb_debug_fused_apply(jfftb_green* green, jfftb_jacobi* jac, int upto, const double* r,
+                            double* out) {
+  return guarded([&] {
+    require(green != nullptr && r != nullptr && out != nullptr, "null argument");
+    jfftb_grid* g = green->grid;
+    require(g->fused, "grid has no fused spectral path");
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    const int64_t n = geo.d * geo.N, ns = spec_elems(g);
+    DevBuf din(sizeof(double) * n), dout(sizeof(double) * n),
+        spec(sizeof(double2) * geo.d * ns);
+    JF_CUDA(cudaMemcpyAsync(din.ptr, r, sizeof(double) * n, cudaMemcpyHostToDevice, g->stream));
+    fused_debug_apply(geo, g->stream, green->blocks, jac ? jac->inv_sqrt : nullptr,
+                      din.as<double>(), dout.as<double>(), spec.as<double2>(), g->twiddle, upto);
+    if (upto >= 5)
+      JF_CUDA(cudaMemcpyAsync(out, dout.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                              g->stream));
+    else
+      JF_CUDA(cudaMemcpyAsync(out, spec.ptr, sizeof(double2) * geo.d * ns,
+                              cudaMemcpyDeviceToHost, g->stream));
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
 int jfftb_profile_start(jfftb_grid* g) {
   return guarded([&] {
     require(g != nullptr, "null grid");

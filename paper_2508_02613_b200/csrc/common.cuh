@@ -345,6 +345,9 @@ void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st
                    const double2* zspec, const double* dinv, double* p, double* x,
                    const double2* tw);
 int64_t fused_component_stride(const Geom& geo);
+void fused_debug_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
+                       const double* dinv, const double* r, double* out, double2* spec,
+                       const double2* tw, int upto);
 
 // stage profile hooks (api.cu); no-ops unless jfftb_profile_start was called
 void prof_mark(jfftb_grid* g);         // event at a stage boundary

@@ -113,11 +113,13 @@ __device__ __forceinline__ void dftR(double2 (&v)[8]) {
 // stay free of shared-memory bank conflicts
 template <int PAD>
 __device__ __forceinline__ int pidx(int k) {
-  return PAD ? k + k / PAD : k;
+  if constexpr (PAD > 0) return k + k / PAD;
+  else return k;
 }
 template <int PAD>
 __host__ __device__ constexpr int padded_len(int L) {
-  return PAD ? L + L / PAD : L;
+  if constexpr (PAD > 0) return L + L / PAD;
+  else return L;
 }
 
 // QFAST: consecutive threads take consecutive sequences (layouts with qs = 1,

@@ -50,7 +50,7 @@ struct FGeom {
   int n1;          // d = 3: axis-1 extent
 };
 
-constexpr int tw_a(int M) { return M >= 512 ? 4 : 8; }
+constexpr int tw_a(int M) { return M >= 1024 ? 4 : (M >= 512 ? 8 : 16); }
 constexpr int tw_b(int L) { return L >= 1024 ? 4 : 8; }
 // one radix-8 butterfly per thread where possible (<= 512 threads)
 constexpr int nt_for(int butterflies) {
@@ -63,85 +63,87 @@ constexpr int nt_for(int butterflies) {
 // FM_APPLY: src = the vector to precondition (not written), F = 1, s-only when
 // `dinv` is given (green-jacobi) else r-only.
 // ---------------------------------------------------------------------------
+// Tiles are TW = 16 real columns (128-byte row segments: at 2 MB strides
+// 64-byte segments reach only ~52% of HBM bandwidth, 128-byte ones ~93%,
+// measured).  Each thread owns PE consecutive (row, column) elements; the
+// inputs stream straight from global in batches, r' goes straight back, and
+// the (up to two) fields are transformed one after the other through one
+// packed smem tile, the s field waiting in registers.
+constexpr int passA_nt(int M) { return nt_for(tw_a(M) * M / 8); }
+
 template <int M, int F, int MODE>
-__global__ void __launch_bounds__(nt_for(F* tw_a(M) * M / 8))
+__global__ void __launch_bounds__(passA_nt(M))
     passA(FGeom g, const PcgState* __restrict__ st, double* __restrict__ r,
           const double* __restrict__ kp, const double* __restrict__ dinv,
           double2* __restrict__ spec, const double2* __restrict__ tw) {
-  constexpr int TW = tw_a(M), FTW = F * TW;
-  constexpr int NT = nt_for(F * TW * M / 8);
-  extern __shared__ double2 sbuf[];  // [k][f * TW + col], k < M
+  constexpr int TW = tw_a(M);
+  constexpr int NT = passA_nt(M);
+  constexpr int RAWN = 2 * M * TW;  // real elements of the tile
+  constexpr int PE = RAWN / NT, CH = PE < 4 ? PE : 4;
+  static_assert(PE * NT == RAWN && PE % CH == 0, "pass A tiling");
+  extern __shared__ double2 sbuf[];  // packed tile [k][col], k < M
   if (MODE != FM_APPLY && st->done) return;
   const int c = blockIdx.y;
   const int64_t col0 = (int64_t)blockIdx.x * TW;
   const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
-  double* rc = r + c * g.N;
-  const double* kc = kp ? kp + c * g.N : nullptr;
-  const double* dc = dinv ? dinv + c * g.N : nullptr;
-  // Stage the raw rows of r, Kp and D^-1/2 (2M x TW doubles each) with
-  // cp.async (full memory-level parallelism, no registers held), pull each
-  // thread's values into registers, then reuse the staging area for the packed
-  // complex tile.
-  double* raw = reinterpret_cast<double*>(sbuf);  // [array][i0][col]
-  constexpr int RAWN = 2 * M * TW;
+  double* rc = r + c * g.N + col0;
+  const double* kc = kp ? kp + c * g.N + col0 : nullptr;
+  const double* dc = dinv ? dinv + c * g.N + col0 : nullptr;
   const bool use_k = MODE == FM_ITER;
   const bool use_d = MODE == FM_APPLY ? dc != nullptr : F == 2;
-  for (int e = threadIdx.x; e < RAWN / 2; e += NT) {  // 16-byte pairs
-    const int i0 = (2 * e) / TW, col = (2 * e) % TW;
-    const int64_t gi = (int64_t)i0 * g.PS + col0 + col;
-    cpa16(raw + 2 * e, rc + gi);
-    if (use_k) cpa16(raw + RAWN + 2 * e, kc + gi);
-    if (use_d) cpa16(raw + 2 * RAWN + 2 * e, dc + gi);
-  }
-  cpa_commit();
-  cpa_wait<0>();
-  __syncthreads();
-  constexpr int PE = M * TW / NT;
-  static_assert(PE * NT == M * TW, "pass A tiling");
-  double v0[PE], v1[PE], s0[PE], s1[PE];
+  double* pk = reinterpret_cast<double*>(sbuf);
+  double sv[PE];  // second field (s = D^-1/2 r'), parked in registers
 #pragma unroll
-  for (int j = 0; j < PE; ++j) {
-    const int e = threadIdx.x + j * NT;
-    const int m = e / TW, col = e % TW;
-    const int l0 = (2 * m) * TW + col, l1 = l0 + TW;
-    double x0 = raw[l0], x1 = raw[l1];
-    if (use_k) {
-      x0 = x0 - alpha * raw[RAWN + l0];
-      x1 = x1 - alpha * raw[RAWN + l1];
-      const int64_t gi = (int64_t)(2 * m) * g.PS + col0 + col;
-      rc[gi] = x0;
-      rc[gi + g.PS] = x1;
-    }
-    if (use_d) {
-      s0[j] = raw[2 * RAWN + l0] * x0;
-      s1[j] = raw[2 * RAWN + l1] * x1;
-    }
-    if (MODE == FM_APPLY && use_d) { x0 = s0[j]; x1 = s1[j]; }
-    v0[j] = x0;
-    v1[j] = x1;
-  }
-  __syncthreads();  // the staging area becomes the packed tile
+  for (int j0 = 0; j0 < PE; j0 += CH) {
+    double a[CH], kv[CH], dv[CH];
 #pragma unroll
-  for (int j = 0; j < PE; ++j) {
-    const int e = threadIdx.x + j * NT;
-    const int m = e / TW, col = e % TW;
-    sbuf[m * FTW + col] = make_double2(v0[j], v1[j]);
-    if (F == 2) sbuf[m * FTW + TW + col] = make_double2(s0[j], s1[j]);
+    for (int j = 0; j < CH; ++j) {
+      const int e = threadIdx.x + (j0 + j) * NT;
+      const int64_t gi = (int64_t)(e / TW) * g.PS + (e % TW);
+      a[j] = rc[gi];
+      if (use_k) kv[j] = kc[gi];
+      if (use_d) dv[j] = __ldg(dc + gi);
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int e = threadIdx.x + (j0 + j) * NT;
+      const int i0 = e / TW, col = e % TW;
+      double xv = a[j];
+      if (use_k) {
+        xv = xv - alpha * kv[j];
+        rc[(int64_t)i0 * g.PS + col] = xv;
+      }
+      const double s = use_d ? dv[j] * xv : xv;
+      sv[j0 + j] = s;
+      // packed complex tile: row i0 = 2m + h is Re (h = 0) / Im (h = 1) of z[m]
+      pk[((i0 >> 1) * TW + col) * 2 + (i0 & 1)] = (MODE == FM_APPLY && use_d) ? s : xv;
+    }
   }
-  __syncthreads();
-  cta_fft<M, FTW, NT, false>(sbuf, FTW, 1, tw);
-  // unpack the packed half-length transform into X[k], k = 0..M
   constexpr int TWS = kTwN / (2 * M);
-  for (int e = threadIdx.x; e < (M + 1) * FTW; e += NT) {
-    const int k = e / FTW, q = e % FTW;
-    const double2 zk = sbuf[(k % M) * FTW + q];
-    const double2 zc = cconj(sbuf[((M - k) % M) * FTW + q]);
-    const double2 fe = cscale(cadd(zk, zc), 0.5);
-    const double2 fo = cscale(csub(zk, zc), 0.5);                   // = i Fo
-    const double2 w = __ldg(tw + ((k * TWS) & (kTwN - 1)));         // e^{-2 pi i k / n0}
-    const double2 x = cadd(fe, cmul(w, mul_mi<false>(fo)));  // Fe + w Fo, Fo = -i fo
-    const int f = q / TW, col = q % TW;
-    spec[(f * g.d + c) * g.CS + (int64_t)k * g.PS + col0 + col] = x;
+#pragma unroll 1
+  for (int f = 0; f < F; ++f) {
+    if (f == 1) {
+      __syncthreads();  // the first field's unpack has read the tile
+#pragma unroll
+      for (int j = 0; j < PE; ++j) {
+        const int e = threadIdx.x + j * NT;
+        const int i0 = e / TW, col = e % TW;
+        pk[((i0 >> 1) * TW + col) * 2 + (i0 & 1)] = sv[j];
+      }
+    }
+    __syncthreads();
+    cta_fft<M, TW, NT, false>(sbuf, TW, 1, tw);
+    // unpack the packed half-length transform into X[k], k = 0..M
+    double2* out = spec + (f * g.d + c) * g.CS + col0;
+    for (int e = threadIdx.x; e < (M + 1) * TW; e += NT) {
+      const int k = e / TW, q = e % TW;
+      const double2 zk = sbuf[(k % M) * TW + q];
+      const double2 zc = cconj(sbuf[((M - k) % M) * TW + q]);
+      const double2 fe = cscale(cadd(zk, zc), 0.5);
+      const double2 fo = cscale(csub(zk, zc), 0.5);                   // = i Fo
+      const double2 w = __ldg(tw + ((k * TWS) & (kTwN - 1)));         // e^{-2 pi i k / n0}
+      out[(int64_t)k * g.PS + q] = cadd(fe, cmul(w, mul_mi<false>(fo)));  // Fe + w Fo
+    }
   }
 }
 
@@ -385,22 +387,9 @@ __global__ void __launch_bounds__(passI_nt(M))
     cpa16(sbuf + e, zc + (int64_t)k * g.PS + col);
   }
   cpa_commit();
-  // the epilogue's D, p, x are fetched now, in flight during the transform
-  constexpr int PE = M * TW / NT;
-  static_assert(PE * NT == M * TW, "pass I tiling");
+  constexpr int RAWN = 2 * M * TW;  // real elements of the tile
   const bool use_d = dinv != nullptr;
-  double dv[PE][2], pv[PE][2], xv[PE][2];
-#pragma unroll
-  for (int j = 0; j < PE; ++j) {
-    const int e = threadIdx.x + j * NT;
-    const int m = e / TW, col = e % TW;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t idx = c * g.N + (int64_t)(2 * m + h) * g.PS + col0 + col;
-      dv[j][h] = use_d ? __ldg(dinv + idx) : 1.0;
-      if (MODE == FM_ITER) { pv[j][h] = p[idx]; xv[j][h] = x[idx]; }
-    }
-  }
+  const int64_t cbase = c * g.N + col0;
   cpa_wait<0>();
   __syncthreads();
   // Z'[k] = (X[k] + conj X[M-k]) + i e^{+2 pi i k / n0} (X[k] - conj X[M-k]),
@@ -422,24 +411,36 @@ __global__ void __launch_bounds__(passI_nt(M))
   const bool done = MODE == FM_ITER ? (st->done != 0) : false;
   const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
   const double beta = MODE == FM_ITER ? st->beta : 0.0;
+  // consecutive threads -> consecutive (row, column): 128-byte row segments;
+  // row i0 = 2m + h is the real (h = 0) / imaginary (h = 1) part of z[m].
+  // D, p, x are loaded in batches of CH elements ahead of their use.
+  const double* zr = reinterpret_cast<const double*>(sbuf);
+  constexpr int PE = RAWN / NT, CH = PE < 4 ? PE : 4;
+  static_assert(PE * NT == RAWN && PE % CH == 0, "pass I tiling");
+#pragma unroll 1
+  for (int j0 = 0; j0 < PE; j0 += CH) {
+    double dv[CH], pv[CH], xv[CH];
 #pragma unroll
-  for (int j = 0; j < PE; ++j) {
-    const int e = threadIdx.x + j * NT;
-    const int m = e / TW, col = e % TW;
-    const double2 z = sbuf[e];
+    for (int j = 0; j < CH; ++j) {
+      const int e = threadIdx.x + (j0 + j) * NT;
+      const int64_t idx = cbase + (int64_t)(e / TW) * g.PS + (e % TW);
+      if (use_d) dv[j] = __ldg(dinv + idx);
+      if (MODE == FM_ITER) { pv[j] = p[idx]; xv[j] = x[idx]; }
+    }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t idx = c * g.N + (int64_t)(2 * m + h) * g.PS + col0 + col;
-      double zz = h ? z.y : z.x;
-      if (use_d) zz = dv[j][h] * zz;
+    for (int j = 0; j < CH; ++j) {
+      const int e = threadIdx.x + (j0 + j) * NT;
+      const int i0 = e / TW, col = e % TW;
+      const int64_t idx = cbase + (int64_t)i0 * g.PS + col;
+      double zz = zr[((i0 >> 1) * TW + col) * 2 + (i0 & 1)];
+      if (use_d) zz = dv[j] * zz;
       if (MODE == FM_APPLY) {
         out[idx] = zz;
       } else if (MODE == FM_INIT) {
         p[idx] = zz;
       } else {
-        const double pold = pv[j][h];
-        x[idx] = xv[j][h] + alpha * pold;
-        if (!done) p[idx] = beta * pold + zz;
+        x[idx] = xv[j] + alpha * pv[j];
+        if (!done) p[idx] = beta * pv[j] + zz;
       }
     }
   }
@@ -470,9 +471,8 @@ template <int M, int F, int MODE>
 void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, const double* kp,
                const double* dinv, double2* spec, const double2* tw) {
   constexpr int TW = tw_a(M);
-  constexpr int NT = nt_for(F * TW * M / 8);
-  // raw staging (3 arrays x 2M x TW doubles) aliases the packed tile
-  const size_t smem = std::max(sizeof(double2) * F * TW * M, sizeof(double) * 3 * 2 * M * TW);
+  constexpr int NT = passA_nt(M);
+  const size_t smem = sizeof(double2) * TW * M;  // one packed field at a time
   auto k = passA<M, F, MODE>;
   static bool attr = false;
   if (!attr) { set_smem(k, smem); attr = true; }
@@ -541,15 +541,14 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
 
 void launchA(const FGeom& g, cudaStream_t s, int F, int mode, const PcgState* st, double* r,
              const double* kp, const double* dinv, double2* spec, const double2* tw) {
+  // one field per launch: two fields in one CTA need either a second 64 KB
+  // tile or the second field parked in registers, and both cost more
+  // occupancy than re-reading r' (3 U) in a second launch saves
+  require(F == 1, "pass A transforms one field per launch");
   const int n0 = g.n0;
-  if (F == 2) {
-    if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 2, FM_ITER>(g, s, st, r, kp, dinv, spec, tw))); }
-    else { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 2, FM_INIT>(g, s, st, r, kp, dinv, spec, tw))); }
-  } else {
-    if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_ITER>(g, s, st, r, kp, dinv, spec, tw))); }
-    else if (mode == FM_INIT) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_INIT>(g, s, st, r, kp, dinv, spec, tw))); }
-    else { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_APPLY>(g, s, st, r, kp, dinv, spec, tw))); }
-  }
+  if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_ITER>(g, s, st, r, kp, dinv, spec, tw))); }
+  else if (mode == FM_INIT) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_INIT>(g, s, st, r, kp, dinv, spec, tw))); }
+  else { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_APPLY>(g, s, st, r, kp, dinv, spec, tw))); }
 }
 void launchB(const FGeom& g, cudaStream_t s, bool inv, bool pred, const PcgState* st,
              double2* spec, int comp0, int ncomp, const double2* tw) {
@@ -614,6 +613,18 @@ void fused_precond_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
   launchC(g, s, 1, FM_APPLY, nullptr, gblocks, gblocks, spec, nullptr, tw);
   if (g.d == 3) launchB(g, s, true, false, nullptr, spec, 0, g.d, tw);
   launchI(g, s, FM_APPLY, nullptr, spec, dinv, nullptr, nullptr, out, tw);
+}
+
+// diagnostic: run the APPLY passes up to `upto` (1 A, 2 B, 3 C, 4 B', 5 I)
+void fused_debug_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
+                       const double* dinv, const double* r, double* out, double2* spec,
+                       const double2* tw, int upto) {
+  const FGeom g = fgeom(geo);
+  launchA(g, s, 1, FM_APPLY, nullptr, const_cast<double*>(r), nullptr, dinv, spec, tw);
+  if (upto >= 2 && g.d == 3) launchB(g, s, false, false, nullptr, spec, 0, g.d, tw);
+  if (upto >= 3) launchC(g, s, 1, FM_APPLY, nullptr, gblocks, gblocks, spec, nullptr, tw);
+  if (upto >= 4 && g.d == 3) launchB(g, s, true, false, nullptr, spec, 0, g.d, tw);
+  if (upto >= 5) launchI(g, s, FM_APPLY, nullptr, spec, dinv, nullptr, nullptr, out, tw);
 }
 
 // ---- the PCG stages (pcg.cu strings them together) ------------------------
