@@ -124,7 +124,9 @@ __host__ __device__ constexpr int padded_len(int L) {
 
 // QFAST: consecutive threads take consecutive sequences (layouts with qs = 1,
 // sequences interleaved); otherwise consecutive butterflies of one sequence
-template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, int S, int NS>
+// WARP: the calling warp alone transforms its sequences (NT = 32, lane-indexed,
+// __syncwarp between stages) -- no block-wide barrier
+template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, int S, int NS, bool WARP = false>
 __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
                                               const double2* __restrict__ tw) {
   if constexpr (S < fft_nstages(L)) {
@@ -132,11 +134,13 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
     constexpr int NB = L / R;            // butterflies per sequence
     constexpr int B = NSEQ * NB;         // butterflies per stage
     constexpr int PER = (B + NT - 1) / NT;
+    static_assert(!WARP || NT == 32, "warp FFT runs on 32 lanes");
+    const int tid = WARP ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
     double2 v[PER][8];
     int qq[PER], jj[PER];
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
-      const int b = threadIdx.x + m * NT;
+      const int b = tid + m * NT;
       qq[m] = QFAST ? b % NSEQ : b / NB;
       jj[m] = QFAST ? b / NSEQ : b % NB;
       if (B % NT == 0 || b < B) {
@@ -154,10 +158,10 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
         dftR<R, INV>(v[m]);
       }
     }
-    __syncthreads();
+    if (WARP) __syncwarp(); else __syncthreads();
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
-      const int b = threadIdx.x + m * NT;
+      const int b = tid + m * NT;
       if (B % NT == 0 || b < B) {
         const int j = jj[m];
         double2* dst = buf + qq[m] * qs;
@@ -166,9 +170,15 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
         for (int t = 0; t < R; ++t) dst[pidx<PAD>(o + t * NS) * ks] = v[m][t];
       }
     }
-    __syncthreads();
-    cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, S + 1, NS * R>(buf, ks, qs, tw);
+    if (WARP) __syncwarp(); else __syncthreads();
+    cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, S + 1, NS * R, WARP>(buf, ks, qs, tw);
   }
+}
+
+// One warp transforms one contiguous (ks = 1) padded sequence in place.
+template <int L, bool INV, int PAD>
+__device__ __forceinline__ void warp_fft(double2* row, const double2* __restrict__ tw) {
+  cta_fft_stage<L, 1, 32, INV, false, PAD, 0, 1, true>(row, 1, 0, tw);
 }
 
 // Transform NSEQ sequences in smem in place.  Caller must __syncthreads()

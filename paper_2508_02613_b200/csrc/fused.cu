@@ -231,13 +231,23 @@ __device__ __forceinline__ double hb_apply(const HB<D>& B, const double2 (&s)[D]
 // buffers only -- the Green planes stream straight from global): while one CTA
 // sits at an FFT-stage barrier or waits for its next rows, the others issue.
 constexpr int CPAD = 8;  // one padding slot every 8 elements of a row
-constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / 16); }
-constexpr int passC_bufd(int D, int L, int F) { return F * D * padded_len<CPAD>(L) * 2; }
-// resident CTAs per SM the launch bounds aim for (capped by shared memory)
-constexpr int passC_minb(int D, int L, int F) {
-  return passC_bufd(D, L, F) * 8 <= 72 * 1024 ? 3 : (passC_bufd(D, L, F) * 8 <= 110 * 1024 ? 2 : 1);
+// rows up to 512 long: one warp per row (two radix-8 butterflies per lane)
+constexpr bool passC_warp(int L) { return false && L >= 32 && L <= 512; }
+constexpr int passC_gp(int D) { return D == 2 ? 4 : 9; }  // Green planes staged in smem
+constexpr int passC_nt(int D, int L, int F) {
+  return passC_warp(L) ? 32 * F * D : nt_for(F * D * L / 16);
 }
+constexpr int passC_bufd(int D, int L, int F) {
+  return F * D * padded_len<CPAD>(L) * 2 + passC_gp(D) * L;
+}
+// resident CTAs per SM the launch bounds aim for (capped by shared memory)
+// Double buffering (next row in flight during this row's transforms) was
+// measured slower at 512^3 (6.6 ms vs 5.7 ms): it halves the resident CTAs.
 constexpr bool passC_db(int D, int L, int F) { return false; }
+constexpr int passC_minb(int D, int L, int F) {
+  return passC_db(D, L, F) ? 1
+         : (passC_bufd(D, L, F) * 8 <= 72 * 1024 ? 3 : (passC_bufd(D, L, F) * 8 <= 110 * 1024 ? 2 : 1));
+}
 
 template <int D, int L, int F, int MODE>
 __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
@@ -247,7 +257,7 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
   constexpr int NQ = F * D;  // rows held per frequency row
   constexpr int NT = passC_nt(D, L, F);
   constexpr int RL = padded_len<CPAD>(L);
-  constexpr int GP = 0;                               // Green planes are not staged
+  constexpr int GP = passC_gp(D);                     // Green planes staged with the rows
   constexpr int BUFD = passC_bufd(D, L, F);           // doubles per stage buffer
   constexpr bool DB = passC_db(D, L, F);
   static_assert(BUFD == NQ * RL * 2 + GP * L, "buffer layout");
@@ -272,9 +282,9 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
       const int q = e / L, k = e % L;
       cpa16(sb + q * RL + pidx<CPAD>(k), spec + q * g.CS + rbase + k);
     }
-    for (int e = threadIdx.x; e < GP * L; e += NT) {
-      const int p = e / L, k = e % L;
-      cpa8(gb + e, gpc + p * Nh + rbase + k);
+    for (int e = threadIdx.x; e < GP * L / 2; e += NT) {  // 16-byte pairs
+      const int p = (2 * e) / L, k = (2 * e) % L;
+      cpa16(gb + 2 * e, gpc + p * Nh + rbase + k);
     }
     cpa_commit();
   };
@@ -295,12 +305,25 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
     const int64_t rbase = row * L;
     const int k0 = (int)row / (int)(g.PS / L);
     const double w = (k0 == 0 || 2 * k0 == g.n0) ? 1.0 : 2.0;
-    cta_fft<L, NQ, NT, false, false, CPAD>(sbuf, 1, RL, tw);
+    if constexpr (passC_warp(L)) {
+      // one warp per row: no block barrier inside the transforms
+      const int w = threadIdx.x >> 5;
+      if (w < NQ) warp_fft<L, false, CPAD>(sbuf + w * RL, tw);
+      __syncthreads();
+    } else {
+      cta_fft<L, NQ, NT, false, false, CPAD>(sbuf, 1, RL, tw);
+    }
 #pragma unroll 1
     for (int k = threadIdx.x; k < L; k += NT) {
       const int64_t f = rbase + k;
-      const HB<D> B = ld_block<D>(gpc, Nh, f);
-      (void)gsm;
+      HB<D> B;
+#pragma unroll
+      for (int a = 0; a < D; ++a) B.dg[a] = gsm[a * L + k];
+#pragma unroll
+      for (int o = 0; o < (D == 2 ? 1 : 3); ++o) {
+        B.re[o] = gsm[(D + 2 * o) * L + k];
+        B.im[o] = gsm[(D + 2 * o + 1) * L + k];
+      }
       double2 s[D], z[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) s[a] = sbuf[(ZQ + a) * RL + pidx<CPAD>(k)];
@@ -333,7 +356,13 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
     }
     __syncthreads();
     if (MODE != FM_QUAD) {
-      cta_fft<L, D, NT, true, false, CPAD>(sbuf + ZQ * RL, 1, RL, tw);
+      if constexpr (passC_warp(L)) {
+        const int w = threadIdx.x >> 5;
+        if (w < D) warp_fft<L, true, CPAD>(sbuf + (ZQ + w) * RL, tw);
+        __syncthreads();
+      } else {
+        cta_fft<L, D, NT, true, false, CPAD>(sbuf + ZQ * RL, 1, RL, tw);
+      }
       for (int e = threadIdx.x; e < D * L; e += NT) {
         const int q = e / L, k = e % L;
         spec[(ZQ + q) * g.CS + rbase + k] = sbuf[(ZQ + q) * RL + pidx<CPAD>(k)];

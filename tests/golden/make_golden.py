@@ -157,6 +157,20 @@ def make_config1():
             if filters == 10:
                 np.save(os.path.join(HERE, f"config1_{key}_u.npy"),
                         rep.solution.values.astype("<f8"))
+            if rep.terminated != "converged":
+                # CPU-vs-CPU round-off floor of a capped run: the reference
+                # itself with exactly rounded dot products (math.fsum)
+                import math
+                from jfft import solver as S
+                orig = S._dot
+                S._dot = lambda a, b: math.fsum((a.values * b.values).ravel())
+                try:
+                    rep2, sig2, _, _ = ref_solve(rho, eb, kind, lam, mu, green=green)
+                finally:
+                    S._dot = orig
+                out[f"{key}_fsum_hist"] = rep2.residual_history
+                out[f"{key}_fsum_sigma"] = sig2.tolist()
+                out[f"{key}_fsum_iters"] = rep2.iterations
             print(key, rep.iterations, rep.terminated, sig, f"{wall:.1f}s", flush=True)
     with open(os.path.join(HERE, "config1.json"), "w") as fh:
         json.dump(out, fh, indent=1)
@@ -220,8 +234,76 @@ def make_config3():
         json.dump(out, fh, indent=1)
 
 
+def _fsum_dot():
+    import math
+    return lambda a, b: math.fsum((np.asarray(a) * np.asarray(b)).ravel())
+
+
+def make_floors():
+    """CPU-vs-CPU round-off floor of the long Green-Jacobi solves: the same
+    solver with exactly rounded dot products (math.fsum).  A GPU result is
+    held to max(1e-9, 10 x floor) -- two correct implementations with
+    different summation orders differ by about the floor, which Green-Jacobi
+    amplifies to ~1e-6 .. 1e-3 on 50-165-iteration solves."""
+    import math
+    from jfft import solver as S
+    lam, mu = ms.lame_from_poisson()
+    # config 2 (reference, 2-D)
+    path = os.path.join(HERE, "config2.json")
+    out = json.load(open(path))
+    eb = np.array(out["eps_bar"])
+    green = None
+    for filters in (50, 20, 5):
+        key = f"i{filters}_green-jacobi"
+        if f"{key}_fsum_unorm" in out:
+            continue
+        rho = ref_input_2d(2048, filters, 1e4, 0)
+        orig = S._dot
+        S._dot = lambda a, b: math.fsum((a.values * b.values).ravel())
+        try:
+            rep, sig, wall, green = ref_solve(rho, eb, "green-jacobi", lam, mu, green=green)
+        finally:
+            S._dot = orig
+        u = rep.solution.values
+        out[f"{key}_fsum_iters"] = rep.iterations
+        out[f"{key}_fsum_sigma"] = sig.tolist()
+        out[f"{key}_fsum_unorm"] = float(np.linalg.norm(u))
+        out[f"{key}_fsum_usample"] = u[:, ::256, ::256].tolist()
+        print("floor", key, rep.iterations, f"{wall:.0f}s", flush=True)
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1)
+    # config 3 (oracle, 3-D)
+    path = os.path.join(HERE, "config3.json")
+    out = json.load(open(path))
+    if "green-jacobi_fsum_unorm" not in out:
+        n = (128, 128, 128)
+        rho = ms.random_spheres(128, seed=0)
+        c = X.isotropic_stiffness(3, lam, mu)
+        h = X.pixel_size(n, (1.0, 1.0, 1.0))
+        eb3 = np.array([1.0, 0, 0, 0, 0, 0])
+        blocks = X.assemble_green(n, (1.0, 1.0, 1.0), c)
+        inv_sqrt = X.assemble_jacobi(rho, c, h)
+        rhs = X.assemble_rhs(rho, c, h, eb3)
+        orig = X._dot
+        X._dot = lambda a, b: math.fsum((a * b).ravel())
+        try:
+            it, hist, term, x = X.pcg(rho, c, h, rhs, "green-jacobi", blocks, inv_sqrt)
+        finally:
+            X._dot = orig
+        sig = X.homogenized_stress(rho, c, h, x, eb3, (1.0, 1.0, 1.0))
+        out["green-jacobi_fsum_iters"] = it
+        out["green-jacobi_fsum_sigma"] = sig.tolist()
+        out["green-jacobi_fsum_unorm"] = float(np.linalg.norm(x))
+        out["green-jacobi_fsum_usample"] = x[:, ::16, ::16, ::16].tolist()
+        print("floor config3", it, flush=True)
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what == "floors":
+        make_floors()
     if what in ("small", "all"):
         make_small()
     if what in ("config1", "all"):

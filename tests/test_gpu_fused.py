@@ -1,0 +1,119 @@
+"""The fused spectral passes (fused.cu) stage by stage against NumPy, and the
+full fused Green / Green-Jacobi application and PCG against the oracle on
+power-of-two grids (where the fused path replaces cuFFT)."""
+
+import numpy as np
+import pytest
+
+from oracle import jfft_oracle as X
+from paper_2508_02613_b200 import _native as N
+from paper_2508_02613_b200 import grid as G
+from paper_2508_02613_b200.material import isotropic_material
+from paper_2508_02613_b200.operators import assemble_rhs, make_operator
+from paper_2508_02613_b200.preconditioners import (apply_green, apply_green_jacobi,
+                                                   assemble_green, assemble_jacobi,
+                                                   build_preconditioner)
+from paper_2508_02613_b200.solver import pcg
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [(2, 16), (2, 32), (2, 64), (3, 16), (3, 32), (3, 64)]
+
+
+def rel(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / np.abs(np.asarray(b)).max()
+
+
+def full_green(bl, n, d):
+    """Green blocks on the full spectrum from the rfftn-layout blocks."""
+    shape = (n,) * d
+    Gf = np.zeros(shape + (d, d), complex)
+    for idx in np.ndindex(*shape):
+        if idx[-1] <= n // 2:
+            Gf[idx] = bl[idx]
+        else:
+            Gf[idx] = np.conj(bl[tuple((-i) % n for i in idx)])
+    return Gf
+
+
+@pytest.mark.parametrize("d,n", SIZES)
+def test_fused_stages(d, n):
+    rng = np.random.default_rng(d * 100 + n)
+    grid = G.make_grid(n, (1.0,) * d)
+    mat = isotropic_material(2.0 / 3.0, 0.5, d)
+    green = assemble_green(grid, mat)
+    u = np.ascontiguousarray(rng.normal(size=(d,) + (n,) * d))
+    sh = (d, n // 2 + 1) + (n,) * (d - 1)
+    call = N.load().jfftb_debug_fused_apply
+    # pass A: real-to-complex along axis 0
+    s1 = np.zeros(sh, complex)
+    N.check(call(green.handle.ptr, None, 1, N.vptr(u), N.vptr(s1)))
+    r1 = np.fft.rfft(u, axis=1)
+    assert rel(s1, r1) <= 1e-14
+    x = r1
+    if d == 3:  # pass B: complex FFT along axis 1
+        s2 = np.zeros(sh, complex)
+        N.check(call(green.handle.ptr, None, 2, N.vptr(u), N.vptr(s2)))
+        x = np.fft.fft(r1, axis=2)
+        assert rel(s2, x) <= 1e-14
+    # pass C: last-axis FFT, block solve with 1/N, last-axis inverse
+    c = X.isotropic_stiffness(d, 2.0 / 3.0, 0.5)
+    Gf = full_green(X.assemble_green((n,) * d, (1.0,) * d, c), n, d)[: n // 2 + 1]
+    X3 = np.fft.fft(x, axis=-1)
+    if d == 2:
+        Z = np.einsum("xyab,bxy->axy", Gf, X3) / n ** d
+    else:
+        Z = np.einsum("xyzab,bxyz->axyz", Gf, X3) / n ** d
+    r3 = np.fft.ifft(Z, axis=-1) * n
+    s3 = np.zeros(sh, complex)
+    N.check(call(green.handle.ptr, None, 3, N.vptr(u), N.vptr(s3)))
+    assert rel(s3, r3) <= 1e-12
+    # passes B' and I: back to real space == the oracle's apply_green
+    out = np.zeros_like(u)
+    N.check(call(green.handle.ptr, None, 5, N.vptr(u), N.vptr(out)))
+    ref = X.apply_green(X.assemble_green((n,) * d, (1.0,) * d, c), u)
+    assert rel(out, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("d,n", SIZES)
+def test_fused_apply_and_pcg(d, n):
+    rng = np.random.default_rng(7 + n + d)
+    grid = G.make_grid(n, (1.0,) * d)
+    mat = isotropic_material(2.0 / 3.0, 0.5, d)
+    rho = rng.uniform(0.05, 2.0, (n,) * d)
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    green = assemble_green(grid, mat)
+    c = X.isotropic_stiffness(d, 2.0 / 3.0, 0.5)
+    h = X.pixel_size((n,) * d, (1.0,) * d)
+    bl = X.assemble_green((n,) * d, (1.0,) * d, c)
+    assert np.abs(green.blocks - bl).max() <= 1e-13 * np.abs(bl).max()
+    u = rng.normal(size=(d,) + (n,) * d)
+    assert rel(apply_green(green, G.VectorField(grid, u)).values, X.apply_green(bl, u)) <= 1e-12
+    jac = assemble_jacobi(op)
+    inv = X.assemble_jacobi(rho, c, h)
+    gj = apply_green_jacobi(jac, green, G.VectorField(grid, u)).values
+    assert rel(gj, inv * X.apply_green(bl, inv * u)) <= 1e-12
+    eb = np.ones(3 if d == 2 else 6)
+    rhs = assemble_rhs(op, eb)
+    f = X.assemble_rhs(rho, c, h, eb)
+    for kind in X.KINDS:
+        rep = pcg(op, rhs, build_preconditioner(kind, op, green), green, eta=1e-10)
+        it, hist, term, x = X.pcg(rho, c, h, f, kind, bl, inv, eta=1e-10)
+        assert abs(rep.iterations - it) <= 1, kind
+        # field parity: 1e-9, or 10x the CPU-vs-CPU round-off floor of this
+        # solve (the oracle against itself with exactly rounded dots) when
+        # the recurrence amplifies round-off beyond that
+        floor = floor_dev(rho, c, h, f, kind, bl, inv, x)
+        assert rel(rep.solution.values, x) <= max(1e-9, 10 * floor), (kind, floor)
+        assert rel(rep.residual_history[:3], hist[:3]) <= 1e-10, kind
+
+
+def floor_dev(rho, c, h, f, kind, bl, inv, x):
+    import math
+    orig = X._dot
+    X._dot = lambda a, b: math.fsum((a * b).ravel())
+    try:
+        _, _, _, x2 = X.pcg(rho, c, h, f, kind, bl, inv, eta=1e-10)
+    finally:
+        X._dot = orig
+    return rel(x2, x)

@@ -202,13 +202,95 @@ def test_config1_parity(golden_dir):
                                - 1.0) <= 1e-9
                 assert rel(rep.residual_history, gold[f"{key}_hist"]) <= 1e-6
             else:
-                # capped run: same status and count; history within the
-                # CPU-vs-CPU floor (parity_floor)
+                # capped run (999 iterations, unconverged): same status and
+                # count; history and stress within 10x the CPU-vs-CPU
+                # round-off floor, i.e. the reference against itself with
+                # exactly rounded dot products (parity_floor)
                 h = np.array(rep.residual_history)
                 hr = np.array(gold[f"{key}_hist"])
-                assert len(h) == len(hr)
-                assert rel(h[:50], hr[:50]) <= 1e-6
-                assert rel(sig, gold[f"{key}_sigma"]) <= 1e-2
+                hf = np.array(gold[f"{key}_fsum_hist"])
+                assert len(h) == len(hr) == len(hf)
+                dev = np.abs(h - hr) / hr
+                floor = np.abs(hf - hr) / hr
+                assert dev.max() <= 10 * floor.max() + 1e-12, (dev.max(), floor.max())
+                sf = np.array(gold[f"{key}_fsum_sigma"])
+                s_floor = np.abs(sf - gold[f"{key}_sigma"]).max()
+                assert np.abs(sig - gold[f"{key}_sigma"]).max() <= 10 * s_floor + 1e-15
+
+
+@pytest.mark.parametrize("filters", [50, 20, 5, 0])
+def test_config2_parity(golden_dir, filters):
+    """BASELINE config 2 (2048^2, pure shear, contrast 1e4) against the
+    reference's own solves (iterations, residual history, homogenized stress,
+    solution norm and a 8 x 8 sample of the field)."""
+    gold = json.load(open(os.path.join(golden_dir, "config2.json")))
+    lam, mu = ms.lame_from_poisson()
+    mat = isotropic_material(lam, mu)
+    rho = ms.bernoulli_smoothed(2048, filters, 1e4, 0)
+    grid = G.make_grid(2048)
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    green = assemble_green(grid, mat)
+    eb = np.array(gold["eps_bar"])
+    rhs = assemble_rhs(op, eb)
+    for kind in ("green", "green-jacobi"):
+        key = f"i{filters}_{kind}"
+        rep = pcg(op, rhs, build_preconditioner(kind, op, green), green)
+        assert rep.terminated == gold[f"{key}_terminated"], key
+        assert abs(rep.iterations - gold[f"{key}_iters"]) <= 1, key
+        sig = homogenized_stress(op, rep.solution, eb)
+        if rep.terminated == CONVERGED:
+            us = rep.solution.values[:, ::256, ::256]
+            ref_us = np.array(gold[f"{key}_usample"])
+            # 1e-9, or 10x the reference's own round-off floor (make_golden
+            # floors) for the long Green-Jacobi solves
+            tol_u = tol_s = 1e-9
+            if f"{key}_fsum_usample" in gold:
+                tol_u = max(1e-9, 10 * rel(np.array(gold[f"{key}_fsum_usample"]), ref_us))
+                tol_s = max(1e-9, 10 * rel(gold[f"{key}_fsum_sigma"], gold[f"{key}_sigma"]))
+            elif kind == "green-jacobi":
+                tol_u = tol_s = None  # floor not generated: status and count only
+            if tol_u is not None:
+                assert rel(sig, gold[f"{key}_sigma"]) <= tol_s, key
+                assert rel(us, ref_us) <= tol_u, (key, tol_u)
+            if kind == "green":
+                assert rel(rep.residual_history, gold[f"{key}_hist"]) <= 1e-6, key
+        else:
+            h = np.array(rep.residual_history)
+            hr = np.array(gold[f"{key}_hist"])
+            assert len(h) == len(hr)
+            # the first iterations agree far below the chaotic late-stage floor
+            assert rel(h[:20], hr[:20]) <= 1e-8, key
+
+
+def test_config3_parity(golden_dir):
+    """BASELINE config 3 (3-D 128^3 spheres, contrast 1e3, eps_xx = 1) against
+    the oracle restatement (no 3-D reference exists)."""
+    path = os.path.join(golden_dir, "config3.json")
+    gold = json.load(open(path))
+    lam, mu = ms.lame_from_poisson()
+    mat = isotropic_material(lam, mu, 3)
+    rho = ms.random_spheres(128, seed=0)
+    assert abs(rho.sum() - gold["rho_sum"]) <= 1e-9 * gold["rho_sum"]
+    grid = G.make_grid(128, (1.0, 1.0, 1.0))
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    green = assemble_green(grid, mat)
+    eb = np.array([1.0, 0, 0, 0, 0, 0])
+    rhs = assemble_rhs(op, eb)
+    for kind in ("green", "green-jacobi"):
+        rep = pcg(op, rhs, build_preconditioner(kind, op, green), green)
+        assert rep.terminated == gold[f"{kind}_terminated"]
+        assert abs(rep.iterations - gold[f"{kind}_iters"]) <= 1, kind
+        sig = homogenized_stress(op, rep.solution, eb)
+        us = rep.solution.values[:, ::16, ::16, ::16]
+        ref_us = np.array(gold[f"{kind}_usample"])
+        tol_u = tol_s = 1e-9
+        if f"{kind}_fsum_usample" in gold:
+            tol_u = max(1e-9, 10 * rel(np.array(gold[f"{kind}_fsum_usample"]), ref_us))
+            tol_s = max(1e-9, 10 * rel(gold[f"{kind}_fsum_sigma"], gold[f"{kind}_sigma"]))
+        elif kind == "green-jacobi":
+            continue  # floor not generated: status and count only
+        assert rel(sig, gold[f"{kind}_sigma"]) <= tol_s, kind
+        assert rel(us, ref_us) <= tol_u, (kind, tol_u)
 
 
 def test_pcg_contract():
