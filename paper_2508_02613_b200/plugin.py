@@ -1,0 +1,85 @@
+"""Drop the GPU path into an imported reference package (``jfft``).
+
+The reference has no plugin registry: its operator API is the set of
+module-level functions re-exported by ``jfft/__init__.py:5-21``, and each
+importing module binds them by name at import time.  This
+rebinds every binding site so that the reference's own experiments, topology
+optimisation, CLI and Newton driver run on libjfftb200:
+
+  preconditioners.{apply_system, make_operator, apply_green, apply_jacobi,
+                   apply_jacobi_half, apply_green_jacobi, assemble_green,
+                   assemble_jacobi, build_preconditioner, Preconditioner}
+  operators.{apply_system, assemble_rhs, total_strain, residual_force,
+             homogenized_stress}
+  solver.{apply_system, residual_force, apply_green, assemble_green,
+          build_preconditioner, pcg}
+  experiments.{assemble_rhs, homogenized_stress, assemble_green,
+                build_preconditioner, pcg}
+  topopt.{assemble_rhs, total_strain, assemble_green, build_preconditioner, pcg}
+  jfft.{...the same names}
+
+``SystemOperator`` objects stay the reference's own (they are plain data);
+the device copy of the density is attached to them lazily.  Solver aborts are
+raised as the reference's ``SolverAbortError``.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import operators as _ops
+from . import preconditioners as _pc
+from . import solver as _solver
+
+_TARGETS = {
+    "preconditioners": ["apply_system", "apply_green", "apply_jacobi", "apply_jacobi_half",
+                        "apply_green_jacobi", "assemble_green", "assemble_jacobi",
+                        "build_preconditioner", "Preconditioner"],
+    "operators": ["apply_system", "assemble_rhs", "total_strain", "residual_force",
+                  "homogenized_stress"],
+    "solver": ["apply_system", "residual_force", "apply_green", "assemble_green",
+               "build_preconditioner", "pcg"],
+    "experiments": ["assemble_rhs", "homogenized_stress", "assemble_green",
+                    "build_preconditioner", "pcg"],
+    "topopt": ["assemble_rhs", "total_strain", "assemble_green", "build_preconditioner", "pcg"],
+    "": ["apply_system", "assemble_rhs", "total_strain", "residual_force", "homogenized_stress",
+         "apply_green", "apply_jacobi", "apply_jacobi_half", "apply_green_jacobi",
+         "assemble_green", "assemble_jacobi", "build_preconditioner", "Preconditioner", "pcg"],
+}
+
+
+def _replacement(name: str, ref_solver):
+    if name == "pcg":
+        def pcg(op, rhs, preconditioner, green, eta=_solver.DEFAULT_ETA_CG,
+                max_iter=_solver.DEFAULT_MAX_ITER):
+            return _solver.pcg(op, rhs, preconditioner, green, eta=eta, max_iter=max_iter,
+                               abort_error=ref_solver.SolverAbortError)
+        pcg.__doc__ = _solver.pcg.__doc__
+        return pcg
+    for mod in (_ops, _pc, _solver):
+        if hasattr(mod, name):
+            return getattr(mod, name)
+    raise AttributeError(name)
+
+
+def plug_into_reference(package: str = "jfft") -> dict:
+    """Rebind the reference's binding sites; returns the originals so that
+    :func:`unplug` can restore them."""
+    ref_solver = importlib.import_module(f"{package}.solver")
+    saved = {}
+    for modname, names in _TARGETS.items():
+        full = package if modname == "" else f"{package}.{modname}"
+        try:
+            mod = importlib.import_module(full)
+        except ImportError:
+            continue
+        for name in names:
+            if hasattr(mod, name):
+                saved[(full, name)] = getattr(mod, name)
+                setattr(mod, name, _replacement(name, ref_solver))
+    return saved
+
+
+def unplug(saved: dict) -> None:
+    for (full, name), obj in saved.items():
+        setattr(importlib.import_module(full), name, obj)

@@ -1,0 +1,106 @@
+"""Host-side logic that runs without a GPU: containers and validation that
+mirror the reference (grid.py, material.py, preconditioners.py), the roofline
+byte model, and the device-free parts of the drop-in layer."""
+
+import numpy as np
+import pytest
+
+from paper_2508_02613_b200 import grid as G
+from paper_2508_02613_b200 import roofline as R
+from paper_2508_02613_b200.material import isotropic_material
+from paper_2508_02613_b200.operators import make_operator, quadrature_weights
+from paper_2508_02613_b200.preconditioners import PRECONDITIONER_KINDS, Preconditioner
+
+
+def test_grid_and_containers_mirror_reference():
+    g = G.make_grid(4)
+    assert g.d == 2 and g.n_nodes == 16 and g.n_quad == 32
+    assert g.node_index(5, -1) == 1 + 4 * 3
+    g3 = G.make_grid(4, (1.0, 2.0, 3.0))
+    assert g3.d == 3 and g3.n_quad == 6 * 64 and g3.cell_volume == 6.0
+    assert G.spectral_shape(g3) == (3, 4, 4, 3)
+    with pytest.raises(ValueError):
+        G.make_grid(1)
+    with pytest.raises(ValueError):
+        G.make_grid(4, (1.0, -1.0))
+    with pytest.raises(ValueError):
+        G.VectorField(g, np.zeros((2, 4, 5)))
+    with pytest.raises(ValueError):
+        G.ScalarField(g, np.zeros((4, 4)), site="edge")
+    q = G.QuadField.zeros(g3)
+    assert q.values.shape == (6, 6, 4, 4, 4)
+    assert quadrature_weights(g3).per_point == pytest.approx(1.0 * 2.0 * 3.0 / 64 / 6)
+
+
+def test_mandel_round_trip():
+    t2 = np.array([[1.0, 0.3], [0.3, -2.0]])
+    assert np.allclose(G.from_mandel(G.to_mandel(t2)), t2)
+    t3 = np.array([[1.0, 0.1, 0.2], [0.1, 2.0, 0.3], [0.2, 0.3, 3.0]])
+    m = G.to_mandel(t3)
+    assert np.allclose(m[3:], np.sqrt(2) * np.array([0.3, 0.2, 0.1]))
+    assert np.allclose(G.from_mandel(m), t3)
+    with pytest.raises(ValueError):
+        G.to_mandel(np.array([[1.0, 0.0], [1.0, 1.0]]))
+
+
+def test_material_and_operator_validation():
+    with pytest.raises(ValueError):
+        isotropic_material(0.0, -1.0)
+    m = isotropic_material(2.0 / 3.0, 0.5)
+    assert np.allclose(m.stiffness @ [1, 1, 1], [7 / 3, 7 / 3, 1])
+    assert m.stiffness_for(3).shape == (6, 6)
+    g = G.make_grid(4)
+    with pytest.raises(ValueError):
+        make_operator(G.ScalarField(g, -np.ones((4, 4))), m)
+    with pytest.raises(ValueError):
+        make_operator(G.ScalarField(g, np.ones((4, 4)), site="node"), m)
+
+
+def test_preconditioner_validation_without_gpu():
+    assert PRECONDITIONER_KINDS == ("none", "green", "jacobi", "green-jacobi")
+    with pytest.raises(ValueError):
+        Preconditioner("spectral")
+    with pytest.raises(ValueError):
+        Preconditioner("green")
+    with pytest.raises(ValueError):
+        Preconditioner("green-jacobi", green=object())
+    assert Preconditioner("none").kind == "none"
+
+
+def test_byte_model():
+    U = 8 * 512 ** 3
+    assert R.algorithmic_bytes("green-jacobi", 3, 512 ** 3) == 55 * U
+    assert R.algorithmic_bytes("green", 3, 512 ** 3) == 43 * U
+    assert R.algorithmic_bytes("green-jacobi", 2, 2048 ** 2) == 37 * 8 * 2048 ** 2
+    assert R.kernel_bytes("stencil", "green-jacobi", 3, 512 ** 3) == 7 * U
+
+
+def test_library_loads_lazily():
+    import sys
+    import paper_2508_02613_b200  # noqa: F401
+    from paper_2508_02613_b200 import _native
+    # importing the package must not load CUDA (fork safety, experiments.py:326-330)
+    assert _native._lib is None or "torch" in sys.modules
+
+
+def test_plugin_rebinds_reference_binding_sites():
+    import os
+    import sys
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not mounted (GPU box)")
+    sys.path.insert(0, ref)
+    import jfft
+    import jfft.experiments
+    import jfft.solver
+    from paper_2508_02613_b200 import plugin, solver
+    orig = jfft.solver.pcg
+    saved = plugin.plug_into_reference("jfft")
+    try:
+        assert jfft.solver.pcg is not orig
+        assert jfft.experiments.assemble_green is plugin._replacement("assemble_green", jfft.solver)
+        assert jfft.preconditioners.apply_system is plugin._replacement("apply_system", jfft.solver)
+        assert len(saved) >= 30
+    finally:
+        plugin.unplug(saved)
+    assert jfft.solver.pcg is orig
