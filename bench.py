@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--iters", type=int, default=20, help="PCG iterations per step")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="use the slab-decomposed solver even at N = 1 (testing)")
     return ap.parse_args()
 
 
@@ -336,6 +338,104 @@ def run_ours(args, rank, world):
     return line
 
 
+def weak_shape(n, world):
+    """Per-GPU work fixed at n^3 nodes: 2 -> (2n, n, n), 4 -> (2n, 2n, n),
+    8 -> (2n)^3 (= BASELINE config 5, 1024^3 on 8 GPUs for n = 512)."""
+    shape = [n, n, n]
+    w, a = world, 0
+    while w > 1:
+        shape[a % 3] *= 2
+        w //= 2
+        a += 1
+    return tuple(shape)
+
+
+def run_slab(args, rank, world):
+    """N > 1: the slab-decomposed solver (paper_2508_02613_b200.slab), NCCL
+    halo / all-to-all / rank-ordered reductions, weak scaling."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_02613_b200 import _native as N
+    from paper_2508_02613_b200 import microstructures as ms
+    from paper_2508_02613_b200 import roofline as R
+    from paper_2508_02613_b200.slab import DeviceBackend, SlabLayout, SlabPCG
+    d, n, gen, eb = WORKLOADS[args.workload]
+    assert d == 3, "slab decomposition is 3-D; 2-D runs as replicas"
+    shape = weak_shape(n, world)
+    lengths = tuple(k / n for k in shape)  # same pixel size as the 1-GPU cell
+    lay = SlabLayout(shape, lengths, world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lam, mu = ms.lame_from_poisson()
+    count = int(round(64 * (shape[0] * shape[1] * shape[2]) / 512 ** 3))
+    rho = ms.crack_discs_device(shape, count=count, seed=0, device=dev,
+                                planes=(lay.plane0, lay.plane0 + lay.L0))
+    solver = SlabPCG(lay, DeviceBackend(dev), rho, lam, mu, kind=args.kind)
+    rhs = solver.assemble_rhs(np.asarray(eb, dtype=np.float64))
+    torch.cuda.synchronize()
+
+    def step():
+        solver.solve(rhs, eta=-1.0, max_iter=args.iters)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
+    N.launch_count(reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    launches = N.launch_count(reset=True)
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    Ng = shape[0] * shape[1] * shape[2]
+    iters_total = args.iters * args.steps
+    value = 3 * Ng * iters_total / (ms_total / 1e3) / 1e9
+    peak, peak_src = peak_hbm()
+    per_iter_ms = ms_total / iters_total
+    alg = R.algorithmic_bytes(args.kind, 3, Ng // world)  # per GPU
+    ach = alg / (per_iter_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "pcg-iteration (slab, per GPU)", "achieved": ach,
+            "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+            "alg_bytes_per_launch": alg, "ms_per_launch": per_iter_ms, "peak_source": peak_src}
+    # e2e: the rhs from pinned host memory and the solution back, every step
+    rhs_h = torch.empty(rhs.shape, dtype=torch.float64, pin_memory=True)
+    rhs_h.copy_(rhs)
+    x_h = torch.empty_like(rhs_h, pin_memory=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(args.e2e_steps, 1)):
+        rhs.copy_(rhs_h, non_blocking=True)
+        _, _, _, x, _ = solver.solve(rhs, eta=-1.0, max_iter=args.iters)
+        x_h.copy_(x)
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_v = 3 * Ng * args.iters * max(args.e2e_steps, 1) / float(te.item()) / 1e9
+    cfg = config_of(args)
+    cfg.update({"shape": list(shape), "parallelism": f"slab{world} (axis-0 slabs, NCCL halo + "
+                "all-to-all + allgather)", "nodes_per_gpu": Ng // world})
+    return {
+        "metric": metric_name(args), "value": value, "unit": "GDOF-it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded crack-disc field on the weak-scaled cell; see DESIGN.md)",
+        "config": cfg, "roofline": roof, "roofline_iteration": roof,
+        "e2e": {"value": e2e_v, "unit": "GDOF-it/s",
+                "h2d_bytes_per_step": int(rhs.numel() * 8 * world),
+                "d2h_bytes_per_step": int(rhs.numel() * 8 * world)},
+        "gpu_launches": int(launches), "clocks": clk,
+    }
+
+
 def run_e2e(args, P, torch, world):
     from paper_2508_02613_b200 import grid as G
     from paper_2508_02613_b200.material import isotropic_material
@@ -387,12 +487,20 @@ def main():
     os.environ["JFFTB_DEVICE"] = str(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    line = run_ours(args, rank, world)
+    if (world > 1 or args.slab) and WORKLOADS[args.workload][0] == 3:
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=0, world_size=1,
+                                    device_id=torch.device("cuda", local))
+        line = run_slab(args, rank, world)
+    else:
+        line = run_ours(args, rank, world)
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline_single(args)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 

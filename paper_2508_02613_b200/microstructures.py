@@ -115,33 +115,45 @@ def crack_discs(n: int = 512, count: int = 64, ell: float = 4.0,
     return out
 
 
-def crack_discs_device(n: int = 512, count: int = 64, ell: float = 4.0, emin: float = 1e-4,
-                       seed: int = 0, device="cuda", out=None):
+def crack_discs_device(n=512, count: int = 64, ell: float = 4.0, emin: float = 1e-4,
+                       seed: int = 0, device="cuda", out=None, planes=None):
     """Device (torch) version of :func:`crack_discs` with the same seeded
-    geometry, for bench-size grids; returns an (n, n, n) float64 tensor."""
+    geometry, for bench-size grids.  ``n`` is an int (cubic) or a shape
+    (n0, n1, n2); ``planes = (lo, hi)`` generates only those axis-0 planes
+    (one slab of a distributed run).  Returns a float64 tensor."""
     import torch
-    centres, normals, radii = crack_discs_params(n, count, seed=seed)
-    ax = torch.arange(n, dtype=torch.float64, device=device) + 0.5
+    shape = (n,) * 3 if isinstance(n, int) else tuple(int(k) for k in n)
+    if isinstance(n, int):
+        centres, normals, radii = crack_discs_params(n, count, seed=seed)
+    else:
+        rng = np.random.default_rng(seed)
+        centres = rng.uniform(0.0, 1.0, (count, 3)) * np.array(shape, dtype=float)
+        normals = rng.normal(size=(count, 3))
+        normals /= np.linalg.norm(normals, axis=1, keepdims=True)
+        radii = rng.uniform(8.0, 32.0, count)
+    lo, hi = planes if planes is not None else (0, shape[0])
+    axes = [torch.arange(k, dtype=torch.float64, device=device) + 0.5 for k in shape]
     if out is None:
-        out = torch.empty((n, n, n), dtype=torch.float64, device=device)
-    chunk = max(1, min(n, (1 << 24) // (n * n)))
-    for i0 in range(0, n, chunk):
-        x0 = ax[i0:i0 + chunk]
-        dmin = torch.full((len(x0), n, n), float("inf"), dtype=torch.float64, device=device)
+        out = torch.empty((hi - lo,) + shape[1:], dtype=torch.float64, device=device)
+    n1, n2 = shape[1], shape[2]
+    chunk = max(1, min(hi - lo, (1 << 24) // (n1 * n2)))
+    for i0 in range(lo, hi, chunk):
+        x0 = axes[0][i0:min(i0 + chunk, hi)]
+        dmin = torch.full((len(x0), n1, n2), float("inf"), dtype=torch.float64, device=device)
         for c, nr, r in zip(centres, normals, radii):
             v0 = x0 - c[0]
-            v0 = (v0 - n * torch.round(v0 / n))[:, None, None]
-            v1 = ax - c[1]
-            v1 = (v1 - n * torch.round(v1 / n))[None, :, None]
-            v2 = ax - c[2]
-            v2 = (v2 - n * torch.round(v2 / n))[None, None, :]
+            v0 = (v0 - shape[0] * torch.round(v0 / shape[0]))[:, None, None]
+            v1 = axes[1] - c[1]
+            v1 = (v1 - n1 * torch.round(v1 / n1))[None, :, None]
+            v2 = axes[2] - c[2]
+            v2 = (v2 - n2 * torch.round(v2 / n2))[None, None, :]
             hgt = v0 * float(nr[0]) + v1 * float(nr[1]) + v2 * float(nr[2])
             rad = torch.sqrt(torch.clamp(v0 * v0 + v1 * v1 + v2 * v2 - hgt * hgt, min=0.0))
             dist = torch.where(rad <= float(r), hgt.abs(),
                                torch.sqrt(hgt * hgt + (rad - float(r)) ** 2))
             torch.minimum(dmin, dist, out=dmin)
         phi = torch.exp(-dmin / ell)
-        out[i0:i0 + chunk] = (1.0 - phi) ** 2 + emin
+        out[i0 - lo:i0 - lo + len(x0)] = (1.0 - phi) ** 2 + emin
     return out
 
 

@@ -1,0 +1,58 @@
+"""The slab-decomposed driver on the GPU (NCCL process group, world size 1 on
+the single-GPU test box): libjfftb200 stencil on the halo-extended slab and
+the frequency-slab Green block solve, against the oracle."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import jfft_oracle as X
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl_group():
+    import torch.distributed as dist
+    if dist.is_initialized():
+        yield
+        return
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [(16, 16, 16), (12, 8, 10), (32, 32, 32)])
+@pytest.mark.parametrize("kind", ["green", "green-jacobi"])
+def test_slab_device_matches_oracle(nccl_group, n, kind):
+    from paper_2508_02613_b200.slab import DeviceBackend, SlabLayout, SlabPCG
+    rng = np.random.default_rng(sum(n))
+    lengths = (1.0, 1.0, 1.0)
+    rho = rng.uniform(0.05, 2.0, n)
+    eb = np.array([1.0, -0.5, 0.3, 0.2, -0.1, 0.4])
+    c = X.isotropic_stiffness(3, 2.0 / 3.0, 0.5)
+    h = X.pixel_size(n, lengths)
+    blocks = X.assemble_green(n, lengths, c)
+    inv = X.assemble_jacobi(rho, c, h)
+    f = X.assemble_rhs(rho, c, h, eb)
+    it, hist, term, x = X.pcg(rho, c, h, f, kind, blocks, inv, eta=1e-10)
+    lay = SlabLayout(n, lengths, 1, 0)
+    dev = torch.device("cuda", 0)
+    solver = SlabPCG(lay, DeviceBackend(dev), torch.from_numpy(rho).to(dev), 2.0 / 3.0, 0.5,
+                     kind=kind)
+    it2, hist2, term2, x2, _ = solver.solve(torch.from_numpy(f).to(dev), eta=1e-10)
+    assert it2 == it and term2 == term
+    assert np.abs(np.array(hist2[:3]) - hist[:3]).max() <= 1e-12 * hist[0]
+    x2 = x2.cpu().numpy()
+    assert np.abs(x2 - x).max() <= 1e-8 * np.abs(x).max()
+    if solver.dinv is not None:
+        assert np.abs(solver.dinv.cpu().numpy() - inv).max() <= 1e-14 * inv.max()
