@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="3d512", choices=sorted(WORKLOADS))
     ap.add_argument("--kind", default="green-jacobi", choices=["green-jacobi", "green"])
-    ap.add_argument("--iters", type=int, default=20, help="PCG iterations per step")
+    ap.add_argument("--iters", type=int, default=50,
+                    help="PCG iterations per step (SURVEY 8d throughput mode: 50 at 512^3)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true",

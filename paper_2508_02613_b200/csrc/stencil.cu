@@ -20,7 +20,10 @@ namespace jfftb {
 
 namespace {
 
-constexpr int BX3 = 32, BY3 = 8;   // 3-D tile (threads), emits 31 x 7 columns
+// 3-D tile (threads), emits 31 x 7 columns (32 x 16 measured slower: 4.05 vs
+// 3.80 ms at 512^3 -- one CTA of 16 warps hides less than two of 8)
+constexpr int BX3 = 32, BY3 = 8;
+constexpr int MINB3 = BY3 <= 8 ? 2 : 1;  // resident CTAs per SM the launch bounds target
 constexpr int BX2 = 128;           // 2-D tile, emits 127 columns
 
 __device__ __forceinline__ int wrapi(int i, int n) {
@@ -93,7 +96,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <int MODE, bool SCALE>
-__global__ void __launch_bounds__(BX3* BY3, 2)
+__global__ void __launch_bounds__(BX3* BY3, MINB3)
     stencil3d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
               double lam0, double mu0, EbarT E, double* __restrict__ out,
               double* __restrict__ partials, int chunk) {
@@ -125,25 +128,28 @@ __global__ void __launch_bounds__(BX3* BY3, 2)
   for (int a = 0; a < 3; ++a) { gs[a] = g.hinv[a]; fs[a] = g.hinv[a]; }
   const double (*Eb)[3] = E.e;
 
-  // async fetch of layer kk (unwrapped, kk >= -1) into ring slot (kk+3)%3
-  auto fetch_u = [&](int kk) {
+  // async fetch of layer kk (unwrapped, -1 <= kk <= n0 + 2) into ring slot
+  // (kk+3)%3; plane wrap by compare (no integer division in the march)
+  auto plane_of = [&](int kk) { return kk < 0 ? kk + n0 : (kk >= n0 ? kk - n0 : kk); };
+  auto slot_of = [](int kk) { return (kk + 3) % 3; };
+  auto fetch_u = [&](int kk, int s) {
     if (!HAS_U) return;
-    const int s = (kk + 3) % 3;
-    const double* ub = u + (int64_t)wrapi(kk, n0) * P;
+    const double* ub = u + (int64_t)plane_of(kk) * P;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const double* ui = ub + i * g.N;
       cp_async8(&U[s][i][ty][tx], ui + col);
-      if (hx) cp_async8(&U[s][i][ty][BX3], ui + colx);
+      if (hx) {
+        cp_async8(&U[s][i][ty][BX3], ui + colx);
+        if (hy) cp_async8(&U[s][i][BY3][BX3], ui + colxy);
+      }
       if (hy) cp_async8(&U[s][i][BY3][tx], ui + coly);
-      if (hx && hy) cp_async8(&U[s][i][BY3][BX3], ui + colxy);
     }
   };
-  auto fetch_r = [&](int kk) {
-    if (rho) cp_async8(&R[(kk + 3) % 3][ty][tx], rho + (int64_t)wrapi(kk, n0) * P + col);
+  auto fetch_r = [&](int kk, int s) {
+    if (rho) cp_async8(&R[s][ty][tx], rho + (int64_t)plane_of(kk) * P + col);
   };
-  auto read_corners = [&](int kk, double (&q)[4][3]) {
-    const int s = (kk + 3) % 3;
+  auto read_corners = [&](int s, double (&q)[4][3]) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       q[0][i] = U[s][i][ty][tx];
@@ -159,28 +165,34 @@ __global__ void __launch_bounds__(BX3* BY3, 2)
 #pragma unroll
     for (int i = 0; i < 3; ++i) uk[q][i] = uk1[q][i] = 0.0;
   // prologue: group A = planes k0-1, k0 and rho(k0-1); group B = plane k0+1, rho(k0)
-  fetch_u(k0 - 1);
-  fetch_u(k0);
-  fetch_r(k0 - 1);
+  int s0 = slot_of(k0 - 1);                   // slot of layer kk (rotates by one)
+  int s1 = s0 == 2 ? 0 : s0 + 1, s2 = s1 == 2 ? 0 : s1 + 1;
+  fetch_u(k0 - 1, s0);
+  fetch_u(k0, s1);
+  fetch_r(k0 - 1, s0);
   cp_async_commit();
-  fetch_u(k0 + 1);
-  fetch_r(k0);
+  fetch_u(k0 + 1, s2);
+  fetch_r(k0, s1);
   cp_async_commit();
   cp_async_wait<1>();
   __syncthreads();
-  if (HAS_U) read_corners(k0 - 1, uk);
+  if (HAS_U) read_corners(s0, uk);
 
   double nxt[3] = {0.0, 0.0, 0.0};
   double csum = 0.0;
-  int64_t obase = (int64_t)wrapi(k0 - 1, n0) * P + col;  // output index of layer kk
+  int64_t obase = (int64_t)plane_of(k0 - 1) * P + col;  // output index of layer kk
   for (int kk = k0 - 1, j = 0; kk < k1; ++kk, ++j) {
     const int b = j & 1;
-    if (HAS_U) read_corners(kk + 1, uk1);
-    const double r = rho ? R[(kk + 3) % 3][ty][tx] : 1.0;
+    // slots: s0 = layer kk (u plane kk, rho kk), s1 = kk + 1, s2 = kk + 2
+    if (HAS_U) read_corners(s1, uk1);
+    const double r = rho ? R[s0][ty][tx] : 1.0;
     // refill: plane kk+3 takes plane kk's slot, rho(kk+2) takes rho(kk-1)'s
-    if (kk + 3 <= k1) fetch_u(kk + 3);
-    if (kk + 2 < k1) fetch_r(kk + 2);
+    if (kk + 3 <= k1) fetch_u(kk + 3, s0);
+    if (kk + 2 < k1) fetch_r(kk + 2, s2);
     cp_async_commit();
+    s0 = s1;
+    s1 = s2;
+    s2 = s2 == 2 ? 0 : s2 + 1;
     double uc[8][3];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -341,7 +353,7 @@ StencilLaunch stencil_config(const Geom& g) {
     // ~16 waves of 2 resident CTAs per SM; marches of >= 16 layers so the
     // per-chunk halo layer stays cheap
     const int bx = (g.n[2] + BX3 - 2) / (BX3 - 1), by = (g.n[1] + BY3 - 2) / (BY3 - 1);
-    int chunks = (16 * 2 * 148 + bx * by - 1) / (bx * by);
+    int chunks = (16 * MINB3 * 148 + bx * by - 1) / (bx * by);
     chunks = std::max(1, std::min(chunks, g.n[0] / 16));
     L.chunk = (g.n[0] + chunks - 1) / chunks;
     chunks = (g.n[0] + L.chunk - 1) / L.chunk;
