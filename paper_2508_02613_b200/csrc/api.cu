@@ -397,9 +397,8 @@ int jfftb_grid_create(int d, const int64_t* n, const double* lengths, int device
   });
 }
 
-int jfftb_grid_destroy(jfftb_grid* g) {
-  return guarded([&] {
-    if (!g) return;
+namespace {
+void grid_free(jfftb_grid* g) {
     DeviceGuard dg(g->device);
     cudaStreamSynchronize(g->stream);
     if (g->plans_ready) {
@@ -417,6 +416,33 @@ int jfftb_grid_destroy(jfftb_grid* g) {
     for (auto e : g->ev_free) cudaEventDestroy(e);
     cudaStreamDestroy(g->own_stream);
     delete g;
+}
+void grid_release(jfftb_grid* g) {
+  if (g->refs.fetch_sub(1) == 1 && g->closed.load()) grid_free(g);
+}
+void op_free(jfftb_op* op) {
+  jfftb_grid* g = op->grid;
+  {
+    DeviceGuard dg(g->device);
+    cudaStreamSynchronize(g->stream);
+    cudaFree(op->rho);
+  }
+  delete op;
+  grid_release(g);
+}
+void op_release(jfftb_op* op) {
+  if (op->refs.fetch_sub(1) == 1 && op->closed.load()) op_free(op);
+}
+}  // namespace
+
+// Destroying a grid (or an operator) that still has live children -- an
+// operator, a Green operator, a Jacobi diagonal -- defers the release to the
+// last child's destroy, so handles may be dropped in any order.
+int jfftb_grid_destroy(jfftb_grid* g) {
+  return guarded([&] {
+    if (!g) return;
+    g->closed.store(true);
+    if (g->refs.load() == 0) grid_free(g);
   });
 }
 
@@ -494,6 +520,7 @@ int jfftb_op_create(jfftb_grid* g, const double* rho, int where, double lambda0,
       throw Error(JFFTB_EINVAL, "negative density");
     }
     auto* op = new jfftb_op();
+    g->refs.fetch_add(1);
     op->grid = g;
     op->rho = own;
     op->lambda0 = lambda0;
@@ -505,10 +532,8 @@ int jfftb_op_create(jfftb_grid* g, const double* rho, int where, double lambda0,
 int jfftb_op_destroy(jfftb_op* op) {
   return guarded([&] {
     if (!op) return;
-    DeviceGuard dg(op->grid->device);
-    cudaStreamSynchronize(op->grid->stream);
-    cudaFree(op->rho);
-    delete op;
+    op->closed.store(true);
+    if (op->refs.load() == 0) op_free(op);
   });
 }
 
@@ -670,6 +695,7 @@ int jfftb_green_create_slab(jfftb_grid* g, double lambda_ref, double mu_ref, int
     launch_green_setup(geo, g->stream, resp.as<double>(), m[0] | (m[1] << 8) | (m[2] << 16),
                        gr->blocks, layout, nfreq);
     JF_CUDA(cudaStreamSynchronize(g->stream));
+    g->refs.fetch_add(1);
     *out = gr;
   });
 }
@@ -700,10 +726,14 @@ int jfftb_green_slab_apply(jfftb_green* green, int kind, double* spec, double* s
 int jfftb_green_destroy(jfftb_green* green) {
   return guarded([&] {
     if (!green) return;
-    DeviceGuard dg(green->grid->device);
-    cudaStreamSynchronize(green->grid->stream);
-    cudaFree(green->blocks);
+    jfftb_grid* g = green->grid;
+    {
+      DeviceGuard dg(g->device);
+      cudaStreamSynchronize(g->stream);
+      cudaFree(green->blocks);
+    }
     delete green;
+    grid_release(g);
   });
 }
 
@@ -794,6 +824,7 @@ int jfftb_jacobi_create(jfftb_op* op, jfftb_jacobi** out) {
       throw;
     }
     auto* j = new jfftb_jacobi();
+    op->refs.fetch_add(1);
     j->op = op;
     j->inv_sqrt = diag;
     *out = j;
@@ -803,10 +834,14 @@ int jfftb_jacobi_create(jfftb_op* op, jfftb_jacobi** out) {
 int jfftb_jacobi_destroy(jfftb_jacobi* jac) {
   return guarded([&] {
     if (!jac) return;
-    DeviceGuard dg(jac->op->grid->device);
-    cudaStreamSynchronize(jac->op->grid->stream);
-    cudaFree(jac->inv_sqrt);
+    jfftb_op* op = jac->op;
+    {
+      DeviceGuard dg(op->grid->device);
+      cudaStreamSynchronize(op->grid->stream);
+      cudaFree(jac->inv_sqrt);
+    }
     delete jac;
+    op_release(op);
   });
 }
 

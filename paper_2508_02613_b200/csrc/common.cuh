@@ -8,6 +8,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <atomic>
 #include <vector>
 
 #include "../../include/jfftb200.h"
@@ -108,10 +109,16 @@ struct jfftb_grid {
   int64_t prof_done_seq = 0;  // iterations of the current solve already collected
   double prof_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int64_t prof_iters = 0;
+  // lifetime: operators and Green operators hold a reference; destroying the
+  // grid first defers the release until the last of them is gone
+  std::atomic<int> refs{0};
+  std::atomic<bool> closed{false};
 };
 
 struct jfftb_op {
   jfftb_grid* grid;
+  std::atomic<int> refs{0};  // Jacobi diagonals built from this operator
+  std::atomic<bool> closed{false};
   double* rho;      // device, N
   double lambda0, mu0;
 };

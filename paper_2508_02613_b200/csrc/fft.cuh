@@ -136,13 +136,24 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
     constexpr int PER = (B + NT - 1) / NT;
     static_assert(!WARP || NT == 32, "warp FFT runs on 32 lanes");
     const int tid = WARP ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+    // SHARE: every butterfly of this thread has the same index j within its
+    // sequence (NT a multiple of NB), so the twiddles are fetched once
+    constexpr bool SHARE = !QFAST && PER > 1 && NT % NB == 0 && B % NT == 0;
     double2 v[PER][8];
     int qq[PER], jj[PER];
+    double2 ws[SHARE ? 8 : 1];
+    if constexpr (SHARE) {
+      if (NS > 1) {
+        const int base = ((tid % NB) % NS) * (kTwN / (NS * R));
+#pragma unroll
+        for (int t = 1; t < R; ++t) ws[SHARE ? t : 0] = __ldg(tw + ((base * t) & (kTwN - 1)));
+      }
+    }
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
       const int b = tid + m * NT;
-      qq[m] = QFAST ? b % NSEQ : b / NB;
-      jj[m] = QFAST ? b / NSEQ : b % NB;
+      qq[m] = QFAST ? b % NSEQ : (SHARE ? tid / NB + m * (NT / NB) : b / NB);
+      jj[m] = QFAST ? b / NSEQ : (SHARE ? tid % NB : b % NB);
       if (B % NT == 0 || b < B) {
         const double2* src = buf + qq[m] * qs;
 #pragma unroll
@@ -151,7 +162,7 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
           const int base = (jj[m] % NS) * (kTwN / (NS * R));
 #pragma unroll
           for (int t = 1; t < R; ++t) {
-            const double2 w = __ldg(tw + ((base * t) & (kTwN - 1)));
+            const double2 w = SHARE ? ws[SHARE ? t : 0] : __ldg(tw + ((base * t) & (kTwN - 1)));
             v[m][t] = INV ? cmulc(v[m][t], w) : cmul(v[m][t], w);
           }
         }

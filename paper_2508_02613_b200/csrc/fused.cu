@@ -273,21 +273,28 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
   constexpr int ZQ = F == 2 ? D : 0;  // first row of the solved spectrum
   auto rows_of = [&](int b) { return sbuf_all + (size_t)b * (BUFD / 2); };
   auto gbl_of = [&](int b) { return reinterpret_cast<double*>(rows_of(b) + NQ * RL); };
-  // stage row `row` (spectra + Green planes) into buffer b with cp.async
-  auto prefetch = [&](int64_t row, int b) {
+  // stage rows [q_lo, q_hi) of spectrum row `row` into buffer b with cp.async,
+  // plus the Green planes when `green`
+  auto prefetch_part = [&](int64_t row, int b, int q_lo, int q_hi, bool green) {
     double2* sb = rows_of(b);
     double* gb = gbl_of(b);
     const int64_t rbase = row * L;
-    for (int e = threadIdx.x; e < NQ * L; e += NT) {
-      const int q = e / L, k = e % L;
+    for (int e = threadIdx.x; e < (q_hi - q_lo) * L; e += NT) {
+      const int q = q_lo + e / L, k = e % L;
       cpa16(sb + q * RL + pidx<CPAD>(k), spec + q * g.CS + rbase + k);
     }
-    for (int e = threadIdx.x; e < GP * L / 2; e += NT) {  // 16-byte pairs
-      const int p = (2 * e) / L, k = (2 * e) % L;
-      cpa16(gb + 2 * e, gpc + p * Nh + rbase + k);
-    }
+    if (green)
+      for (int e = threadIdx.x; e < GP * L / 2; e += NT) {  // 16-byte pairs
+        const int p = (2 * e) / L, k = (2 * e) % L;
+        cpa16(gb + 2 * e, gpc + p * Nh + rbase + k);
+      }
     cpa_commit();
   };
+  auto prefetch = [&](int64_t row, int b) { prefetch_part(row, b, 0, NQ, true); };
+  // Single-buffered: the Green planes and the r^ rows are dead once the block
+  // solve is done, so the next row's copies of them are issued before the
+  // inverse transform; the s^ rows (overwritten by z^) follow the store.
+  constexpr bool EARLY = !DB && MODE != FM_QUAD;
   int64_t row = blockIdx.x;
   if (row < rows) prefetch(row, 0);
   for (int it = 0; row < rows; ++it, row += gridDim.x) {
@@ -355,6 +362,8 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
         for (int a = 0; a < D; ++a) sbuf[(ZQ + a) * RL + pidx<CPAD>(k)] = cscale(z[a], invN);
     }
     __syncthreads();
+    const bool more = row + gridDim.x < rows;
+    if (EARLY && more) prefetch_part(row + gridDim.x, 0, 0, ZQ, true);
     if (MODE != FM_QUAD) {
       if constexpr (passC_warp(L)) {
         const int w = threadIdx.x >> 5;
@@ -369,7 +378,8 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
       }
       __syncthreads();
     }
-    if (!DB && row + gridDim.x < rows) prefetch(row + gridDim.x, 0);
+    if (EARLY && more) prefetch_part(row + gridDim.x, 0, ZQ, NQ, false);
+    else if (!DB && more) prefetch(row + gridDim.x, 0);
   }
   cpa_wait<0>();
   if (MODE != FM_APPLY) {

@@ -176,7 +176,11 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   cp_async_commit();
   cp_async_wait<1>();
   __syncthreads();
-  if (HAS_U) read_corners(s0, uk);
+  if (HAS_U) {
+    read_corners(s0, uk);
+    // the first layer refills slot s0: every warp must be done reading it
+    __syncthreads();
+  }
 
   double nxt[3] = {0.0, 0.0, 0.0};
   double csum = 0.0;

@@ -1,0 +1,69 @@
+"""Run-to-run determinism of the device path and handle lifetime.
+
+Every reduction in the library has a fixed order (kRedBlocks partials, fixed
+stencil/pass grids), so repeated applications and solves on the same inputs
+must agree bit for bit.  The grid is large enough for the stencil to march in
+several axis-0 chunks over several waves -- the regime where a missing
+barrier between the march prologue and the first ring refill once let a fast
+warp overwrite a plane its neighbours were still reading (rare, so the
+operator is applied many times).
+"""
+
+import numpy as np
+import pytest
+
+from paper_2508_02613_b200 import _native as N
+from paper_2508_02613_b200 import grid as G
+from paper_2508_02613_b200.material import isotropic_material
+from paper_2508_02613_b200.operators import apply_system, assemble_rhs, make_operator
+from paper_2508_02613_b200.preconditioners import assemble_green, build_preconditioner
+from paper_2508_02613_b200.solver import pcg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def problem():
+    n = 128
+    rng = np.random.default_rng(3)
+    grid = G.make_grid(n, (1.0, 1.0, 1.0))
+    mat = isotropic_material(2.0 / 3.0, 0.5, 3)
+    op = make_operator(G.ScalarField(grid, rng.uniform(1e-3, 1.0, (n,) * 3)), mat)
+    green = assemble_green(grid, mat)
+    u = G.VectorField(grid, rng.standard_normal((3, n, n, n)))
+    return grid, op, green, u
+
+
+def test_stencil_is_deterministic(problem):
+    _, op, _, u = problem
+    ref = apply_system(op, u).values.copy()
+    for i in range(150):
+        assert np.array_equal(apply_system(op, u).values, ref), i
+
+
+@pytest.mark.parametrize("kind", ["none", "green", "green-jacobi"])
+def test_pcg_is_deterministic(problem, kind):
+    _, op, green, _ = problem
+    rhs = assemble_rhs(op, np.array([1.0, 0.0, 0.0, 0.0, 0.0, 0.0]))
+    pc = build_preconditioner(kind, op, green)
+    ref = pcg(op, rhs, pc, green, eta=-1.0, max_iter=40)
+    for _ in range(4):
+        rep = pcg(op, rhs, pc, green, eta=-1.0, max_iter=40)
+        assert rep.residual_history == ref.residual_history, kind
+        assert np.array_equal(rep.solution.values, ref.solution.values), kind
+
+
+def test_handles_may_be_destroyed_in_any_order():
+    """Grid first, then its operator, Green operator and Jacobi diagonal."""
+    lib = N.load()
+    gh = N.GridHandle(3, (16, 16, 16), (1.0, 1.0, 1.0))
+    rho = np.ones((16, 16, 16))
+    op = N.OpHandle(gh, rho, 2.0 / 3.0, 0.5)
+    green = N.GreenHandle(gh, 2.0 / 3.0, 0.5)
+    jac = N.JacobiHandle(op)
+    assert lib.jfftb_grid_destroy(gh.ptr) == N.OK
+    gh.ptr = None
+    # the operator goes before the Jacobi diagonal that still refers to it
+    for h in (op, green, jac):
+        assert getattr(lib, h._destroy)(h.ptr) == N.OK
+        h.ptr = None
