@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(passA_nt(M))
   constexpr int TW = tw_a(M);
   constexpr int NT = passA_nt(M);
   constexpr int RAWN = 2 * M * TW;  // real elements of the tile
-  constexpr int PE = RAWN / NT, CH = PE < 4 ? PE : 4;
+  constexpr int PE = RAWN / NT, CH = PE < 8 ? PE : 8;
   static_assert(PE * NT == RAWN && PE % CH == 0, "pass A tiling");
   extern __shared__ double2 sbuf[];  // packed tile [k][col], k < M
   if (MODE != FM_APPLY && st->done) return;
@@ -407,9 +407,13 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
 //   FM_APPLY: out = Dz           (D = D^-1/2 for green-jacobi, identity for green)
 // ---------------------------------------------------------------------------
 constexpr int passI_nt(int M) { return nt_for(tw_a(M) * M / 4); }
+// two resident CTAs per SM where the tile fits twice (register cap 64)
+constexpr int passI_minb(int M) {
+  return 2 * (size_t)16 * tw_a(M) * (M + 1) <= 200 * 1024 && passI_nt(M) >= 512 ? 2 : 1;
+}
 
 template <int M, int MODE>
-__global__ void __launch_bounds__(passI_nt(M))
+__global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
     passI(FGeom g, const PcgState* __restrict__ st, const double2* __restrict__ zspec,
           const double* __restrict__ dinv, double* __restrict__ p, double* __restrict__ x,
           double* __restrict__ out, const double2* __restrict__ tw) {
