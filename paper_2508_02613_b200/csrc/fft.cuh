@@ -126,10 +126,18 @@ __host__ __device__ constexpr int padded_len(int L) {
 // sequences interleaved); otherwise consecutive butterflies of one sequence
 // WARP: the calling warp alone transforms its sequences (NT = 32, lane-indexed,
 // __syncwarp between stages) -- no block-wide barrier
-template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, int S, int NS, bool WARP = false>
+// GIN: the first stage reads its inputs from global memory (sequence q
+// contiguous at gin + q * gqs) instead of buf; GOUT: the last stage writes
+// its outputs to gout + q * gqs (no trailing barrier -- buf is only read).
+template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, int S, int NS, bool WARP = false,
+          bool GIN = false, bool GOUT = false>
 __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
-                                              const double2* __restrict__ tw) {
+                                              const double2* __restrict__ tw,
+                                              const double2* gin = nullptr,
+                                              double2* gout = nullptr, int64_t gqs = 0) {
   if constexpr (S < fft_nstages(L)) {
+    constexpr bool FROM_G = GIN && S == 0;
+    constexpr bool TO_G = GOUT && S + 1 == fft_nstages(L);
     constexpr int R = fft_radix(L, S);
     constexpr int NB = L / R;            // butterflies per sequence
     constexpr int B = NSEQ * NB;         // butterflies per stage
@@ -155,9 +163,15 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
       qq[m] = QFAST ? b % NSEQ : (SHARE ? tid / NB + m * (NT / NB) : b / NB);
       jj[m] = QFAST ? b / NSEQ : (SHARE ? tid % NB : b % NB);
       if (B % NT == 0 || b < B) {
-        const double2* src = buf + qq[m] * qs;
+        if constexpr (FROM_G) {
+          const double2* src = gin + qq[m] * gqs;
 #pragma unroll
-        for (int t = 0; t < R; ++t) v[m][t] = src[pidx<PAD>(jj[m] + t * NB) * ks];
+          for (int t = 0; t < R; ++t) v[m][t] = src[jj[m] + t * NB];
+        } else {
+          const double2* src = buf + qq[m] * qs;
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[m][t] = src[pidx<PAD>(jj[m] + t * NB) * ks];
+        }
         if (NS > 1) {
           const int base = (jj[m] % NS) * (kTwN / (NS * R));
 #pragma unroll
@@ -169,27 +183,32 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
         dftR<R, INV>(v[m]);
       }
     }
-    if (WARP) __syncwarp(); else __syncthreads();
+    if constexpr (!FROM_G) {
+      if (WARP) __syncwarp(); else __syncthreads();
+    }
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
       const int b = tid + m * NT;
       if (B % NT == 0 || b < B) {
         const int j = jj[m];
-        double2* dst = buf + qq[m] * qs;
         const int o = (j / NS) * NS * R + (j % NS);
+        if constexpr (TO_G) {
+          double2* dst = gout + qq[m] * gqs;
 #pragma unroll
-        for (int t = 0; t < R; ++t) dst[pidx<PAD>(o + t * NS) * ks] = v[m][t];
+          for (int t = 0; t < R; ++t) dst[o + t * NS] = v[m][t];
+        } else {
+          double2* dst = buf + qq[m] * qs;
+#pragma unroll
+          for (int t = 0; t < R; ++t) dst[pidx<PAD>(o + t * NS) * ks] = v[m][t];
+        }
       }
     }
-    if (WARP) __syncwarp(); else __syncthreads();
-    cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, S + 1, NS * R, WARP>(buf, ks, qs, tw);
+    if constexpr (!TO_G) {
+      if (WARP) __syncwarp(); else __syncthreads();
+    }
+    cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, S + 1, NS * R, WARP, GIN, GOUT>(buf, ks, qs, tw,
+                                                                             gin, gout, gqs);
   }
-}
-
-// One warp transforms one contiguous (ks = 1) padded sequence in place.
-template <int L, bool INV, int PAD>
-__device__ __forceinline__ void warp_fft(double2* row, const double2* __restrict__ tw) {
-  cta_fft_stage<L, 1, 32, INV, false, PAD, 0, 1, true>(row, 1, 0, tw);
 }
 
 // Transform NSEQ sequences in smem in place.  Caller must __syncthreads()
@@ -198,6 +217,16 @@ template <int L, int NSEQ, int NT, bool INV, bool QFAST = true, int PAD = 0>
 __device__ __forceinline__ void cta_fft(double2* buf, int ks, int qs,
                                         const double2* __restrict__ tw) {
   cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, 0, 1>(buf, ks, qs, tw);
+}
+// Contiguous rows (ks = 1, row q at buf + q * qs) transformed on the way
+// between global memory and shared memory: GIN reads the inputs from
+// gin + q * gqs (no prior smem staging; caller barriers before, as buf is
+// written by the first stage), GOUT writes the outputs to gout + q * gqs.
+template <int L, int NSEQ, int NT, bool INV, int PAD, bool GIN, bool GOUT>
+__device__ __forceinline__ void cta_fft_io(double2* buf, int qs, const double2* __restrict__ tw,
+                                           const double2* gin, double2* gout, int64_t gqs) {
+  cta_fft_stage<L, NSEQ, NT, INV, false, PAD, 0, 1, false, GIN, GOUT>(buf, 1, qs, tw, gin, gout,
+                                                                      gqs);
 }
 
 // exp(-2 pi i j / 4096), j < 4096

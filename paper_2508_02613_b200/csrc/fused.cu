@@ -227,26 +227,27 @@ __device__ __forceinline__ double hb_apply(const HB<D>& B, const double2 (&s)[D]
   return q;
 }
 
-// Several small CTAs per SM (two radix-8 butterflies per thread per stage, row
-// buffers only -- the Green planes stream straight from global): while one CTA
-// sits at an FFT-stage barrier or waits for its next rows, the others issue.
+// Two CTAs per SM, two radix-8 butterflies per thread per stage.  The rows
+// never take a staging trip through shared memory: the first forward stage
+// reads its butterfly inputs straight from global memory (coalesced: thread j
+// of a sequence takes elements j + t L/8) and the last inverse stage writes
+// straight back, so a row-set costs two shared-memory round trips per
+// transform instead of four.  The Green planes of the next row-set are copied
+// to shared memory with cp.async while the current inverse transform runs.
 constexpr int CPAD = 8;  // one padding slot every 8 elements of a row
-// rows up to 512 long: one warp per row (two radix-8 butterflies per lane)
-constexpr bool passC_warp(int L) { return false && L >= 32 && L <= 512; }
-constexpr int passC_gp(int D) { return D == 2 ? 4 : 9; }  // Green planes staged in smem
-constexpr int passC_nt(int D, int L, int F) {
-  return passC_warp(L) ? 32 * F * D : nt_for(F * D * L / 16);
-}
+// Green planes staged in smem (GSTAGE) or read straight from global in the solve
+constexpr bool kGStage = true;
+constexpr int passC_gp(int D) { return kGStage ? (D == 2 ? 4 : 9) : 0; }
+constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / 16); }
 constexpr int passC_bufd(int D, int L, int F) {
   return F * D * padded_len<CPAD>(L) * 2 + passC_gp(D) * L;
 }
-// resident CTAs per SM the launch bounds aim for (capped by shared memory)
-// Double buffering (next row in flight during this row's transforms) was
-// measured slower at 512^3 (6.6 ms vs 5.7 ms): it halves the resident CTAs.
-constexpr bool passC_db(int D, int L, int F) { return false; }
+// resident CTAs per SM the launch bounds aim for (capped by shared memory).
+// Double buffering the rows (next row-set in flight during this one's
+// transforms) was measured slower at 512^3 (6.6 ms vs 5.7 ms): it halves the
+// resident CTAs.
 constexpr int passC_minb(int D, int L, int F) {
-  return passC_db(D, L, F) ? 1
-         : (passC_bufd(D, L, F) * 8 <= 72 * 1024 ? 3 : (passC_bufd(D, L, F) * 8 <= 110 * 1024 ? 2 : 1));
+  return passC_bufd(D, L, F) * 8 <= 72 * 1024 ? 3 : (passC_bufd(D, L, F) * 8 <= 110 * 1024 ? 2 : 1);
 }
 
 template <int D, int L, int F, int MODE>
@@ -257,12 +258,11 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
   constexpr int NQ = F * D;  // rows held per frequency row
   constexpr int NT = passC_nt(D, L, F);
   constexpr int RL = padded_len<CPAD>(L);
-  constexpr int GP = passC_gp(D);                     // Green planes staged with the rows
-  constexpr int BUFD = passC_bufd(D, L, F);           // doubles per stage buffer
-  constexpr bool DB = passC_db(D, L, F);
+  constexpr int GP = passC_gp(D);            // Green planes staged with the rows
+  constexpr int BUFD = passC_bufd(D, L, F);  // doubles of shared memory
   static_assert(BUFD == NQ * RL * 2 + GP * L, "buffer layout");
-  // [buf][ rows: NQ x RL double2 | Green planes: GP x L double ]
-  extern __shared__ double2 sbuf_all[];
+  // [ rows: NQ x RL double2 | Green planes: GP x L double ]
+  extern __shared__ double2 sbuf[];
   __shared__ double red[64];
   if (MODE != FM_APPLY && st->done) return;
   static_assert(MODE != FM_QUAD || F == 1, "quad-only pass holds one spectrum");
@@ -271,65 +271,41 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
   const int64_t Nh = g.CS;
   double q0 = 0.0, q1 = 0.0;
   constexpr int ZQ = F == 2 ? D : 0;  // first row of the solved spectrum
-  auto rows_of = [&](int b) { return sbuf_all + (size_t)b * (BUFD / 2); };
-  auto gbl_of = [&](int b) { return reinterpret_cast<double*>(rows_of(b) + NQ * RL); };
-  // stage rows [q_lo, q_hi) of spectrum row `row` into buffer b with cp.async,
-  // plus the Green planes when `green`
-  auto prefetch_part = [&](int64_t row, int b, int q_lo, int q_hi, bool green) {
-    double2* sb = rows_of(b);
-    double* gb = gbl_of(b);
+  double* gsm = reinterpret_cast<double*>(sbuf + NQ * RL);
+  auto prefetch_green = [&](int64_t row) {
+    if (!kGStage) return;
     const int64_t rbase = row * L;
-    for (int e = threadIdx.x; e < (q_hi - q_lo) * L; e += NT) {
-      const int q = q_lo + e / L, k = e % L;
-      cpa16(sb + q * RL + pidx<CPAD>(k), spec + q * g.CS + rbase + k);
+    for (int e = threadIdx.x; e < GP * L / 2; e += NT) {  // 16-byte pairs
+      const int p = (2 * e) / L, k = (2 * e) % L;
+      cpa16(gsm + 2 * e, gpc + p * Nh + rbase + k);
     }
-    if (green)
-      for (int e = threadIdx.x; e < GP * L / 2; e += NT) {  // 16-byte pairs
-        const int p = (2 * e) / L, k = (2 * e) % L;
-        cpa16(gb + 2 * e, gpc + p * Nh + rbase + k);
-      }
     cpa_commit();
   };
-  auto prefetch = [&](int64_t row, int b) { prefetch_part(row, b, 0, NQ, true); };
-  // Single-buffered: the Green planes and the r^ rows are dead once the block
-  // solve is done, so the next row's copies of them are issued before the
-  // inverse transform; the s^ rows (overwritten by z^) follow the store.
-  constexpr bool EARLY = !DB && MODE != FM_QUAD;
   int64_t row = blockIdx.x;
-  if (row < rows) prefetch(row, 0);
-  for (int it = 0; row < rows; ++it, row += gridDim.x) {
-    const int b = DB ? (it & 1) : 0;
-    if (DB) {
-      if (row + gridDim.x < rows) prefetch(row + gridDim.x, b ^ 1);
-      else cpa_commit();
-      cpa_wait<1>();
-    } else {
-      cpa_wait<0>();
-    }
-    __syncthreads();
-    double2* sbuf = rows_of(b);
-    const double* gsm = gbl_of(b);
+  if (row < rows) prefetch_green(row);
+  for (; row < rows; row += gridDim.x) {
     const int64_t rbase = row * L;
     const int k0 = (int)row / (int)(g.PS / L);
     const double w = (k0 == 0 || 2 * k0 == g.n0) ? 1.0 : 2.0;
-    if constexpr (passC_warp(L)) {
-      // one warp per row: no block barrier inside the transforms
-      const int w = threadIdx.x >> 5;
-      if (w < NQ) warp_fft<L, false, CPAD>(sbuf + w * RL, tw);
-      __syncthreads();
-    } else {
-      cta_fft<L, NQ, NT, false, false, CPAD>(sbuf, 1, RL, tw);
-    }
+    // forward: global rows -> (stage 1) -> shared; barrier-separated from the
+    // previous row-set's last shared-memory reads by the loop-end barrier
+    cta_fft_io<L, NQ, NT, false, CPAD, true, false>(sbuf, RL, tw, spec + rbase, nullptr, g.CS);
+    cpa_wait<0>();  // this row-set's Green planes
+    __syncthreads();
 #pragma unroll 1
     for (int k = threadIdx.x; k < L; k += NT) {
       const int64_t f = rbase + k;
       HB<D> B;
+      if constexpr (kGStage) {
 #pragma unroll
-      for (int a = 0; a < D; ++a) B.dg[a] = gsm[a * L + k];
+        for (int a = 0; a < D; ++a) B.dg[a] = gsm[a * L + k];
 #pragma unroll
-      for (int o = 0; o < (D == 2 ? 1 : 3); ++o) {
-        B.re[o] = gsm[(D + 2 * o) * L + k];
-        B.im[o] = gsm[(D + 2 * o + 1) * L + k];
+        for (int o = 0; o < (D == 2 ? 1 : 3); ++o) {
+          B.re[o] = gsm[(D + 2 * o) * L + k];
+          B.im[o] = gsm[(D + 2 * o + 1) * L + k];
+        }
+      } else {
+        B = ld_block<D>(gpc, Nh, f);
       }
       double2 s[D], z[D];
 #pragma unroll
@@ -356,30 +332,16 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
           }
         }
       }
-#pragma unroll
       if (MODE != FM_QUAD)
 #pragma unroll
         for (int a = 0; a < D; ++a) sbuf[(ZQ + a) * RL + pidx<CPAD>(k)] = cscale(z[a], invN);
     }
+    __syncthreads();  // block solve done: Green planes and r^ rows are free
+    if (row + gridDim.x < rows) prefetch_green(row + gridDim.x);
+    if (MODE != FM_QUAD)
+      cta_fft_io<L, D, NT, true, CPAD, false, true>(sbuf + ZQ * RL, RL, tw, nullptr,
+                                                    spec + ZQ * g.CS + rbase, g.CS);
     __syncthreads();
-    const bool more = row + gridDim.x < rows;
-    if (EARLY && more) prefetch_part(row + gridDim.x, 0, 0, ZQ, true);
-    if (MODE != FM_QUAD) {
-      if constexpr (passC_warp(L)) {
-        const int w = threadIdx.x >> 5;
-        if (w < D) warp_fft<L, true, CPAD>(sbuf + (ZQ + w) * RL, tw);
-        __syncthreads();
-      } else {
-        cta_fft<L, D, NT, true, false, CPAD>(sbuf + ZQ * RL, 1, RL, tw);
-      }
-      for (int e = threadIdx.x; e < D * L; e += NT) {
-        const int q = e / L, k = e % L;
-        spec[(ZQ + q) * g.CS + rbase + k] = sbuf[(ZQ + q) * RL + pidx<CPAD>(k)];
-      }
-      __syncthreads();
-    }
-    if (EARLY && more) prefetch_part(row + gridDim.x, 0, ZQ, NQ, false);
-    else if (!DB && more) prefetch(row + gridDim.x, 0);
   }
   cpa_wait<0>();
   if (MODE != FM_APPLY) {
@@ -541,8 +503,7 @@ int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* 
               const double* gterm, double2* spec, double* partials, const double2* tw) {
   constexpr int NT = passC_nt(D, L, F);
   constexpr int BUFD = passC_bufd(D, L, F);
-  constexpr bool DB = passC_db(D, L, F);
-  const size_t smem = sizeof(double) * BUFD * (DB ? 2 : 1);
+  const size_t smem = sizeof(double) * BUFD;
   auto k = passC<D, L, F, MODE>;
   static int per_sm = -1;  // per instantiation
   if (per_sm < 0) {
