@@ -134,7 +134,8 @@ template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, int S, int NS,
 __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
                                               const double2* __restrict__ tw,
                                               const double2* gin = nullptr,
-                                              double2* gout = nullptr, int64_t gqs = 0) {
+                                              double2* gout = nullptr, int64_t gqs = 0,
+                                              int64_t gks = 1) {
   if constexpr (S < fft_nstages(L)) {
     constexpr bool FROM_G = GIN && S == 0;
     constexpr bool TO_G = GOUT && S + 1 == fft_nstages(L);
@@ -166,7 +167,7 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
         if constexpr (FROM_G) {
           const double2* src = gin + qq[m] * gqs;
 #pragma unroll
-          for (int t = 0; t < R; ++t) v[m][t] = src[jj[m] + t * NB];
+          for (int t = 0; t < R; ++t) v[m][t] = src[(jj[m] + t * NB) * gks];
         } else {
           const double2* src = buf + qq[m] * qs;
 #pragma unroll
@@ -195,7 +196,7 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
         if constexpr (TO_G) {
           double2* dst = gout + qq[m] * gqs;
 #pragma unroll
-          for (int t = 0; t < R; ++t) dst[o + t * NS] = v[m][t];
+          for (int t = 0; t < R; ++t) dst[(o + t * NS) * gks] = v[m][t];
         } else {
           double2* dst = buf + qq[m] * qs;
 #pragma unroll
@@ -207,7 +208,7 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
       if (WARP) __syncwarp(); else __syncthreads();
     }
     cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, S + 1, NS * R, WARP, GIN, GOUT>(buf, ks, qs, tw,
-                                                                             gin, gout, gqs);
+                                                                             gin, gout, gqs, gks);
   }
 }
 
@@ -218,15 +219,16 @@ __device__ __forceinline__ void cta_fft(double2* buf, int ks, int qs,
                                         const double2* __restrict__ tw) {
   cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, 0, 1>(buf, ks, qs, tw);
 }
-// Contiguous rows (ks = 1, row q at buf + q * qs) transformed on the way
-// between global memory and shared memory: GIN reads the inputs from
-// gin + q * gqs (no prior smem staging; caller barriers before, as buf is
-// written by the first stage), GOUT writes the outputs to gout + q * gqs.
-template <int L, int NSEQ, int NT, bool INV, int PAD, bool GIN, bool GOUT>
-__device__ __forceinline__ void cta_fft_io(double2* buf, int qs, const double2* __restrict__ tw,
-                                           const double2* gin, double2* gout, int64_t gqs) {
-  cta_fft_stage<L, NSEQ, NT, INV, false, PAD, 0, 1, false, GIN, GOUT>(buf, 1, qs, tw, gin, gout,
-                                                                      gqs);
+// Sequences transformed on the way between global and shared memory: GIN
+// reads the first stage's inputs from gin + q * gqs + k * gks (no prior smem
+// staging; the caller barriers before, as buf is written by the first
+// stage), GOUT writes the last stage's outputs to gout + q * gqs + k * gks.
+template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, bool GIN, bool GOUT>
+__device__ __forceinline__ void cta_fft_io(double2* buf, int ks, int qs,
+                                           const double2* __restrict__ tw, const double2* gin,
+                                           double2* gout, int64_t gqs, int64_t gks) {
+  cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, 0, 1, false, GIN, GOUT>(buf, ks, qs, tw, gin, gout,
+                                                                      gqs, gks);
 }
 
 // exp(-2 pi i j / 4096), j < 4096

@@ -163,18 +163,10 @@ __global__ void __launch_bounds__(nt_for(tw_b(L) * L / 8))
   const int k0 = blockIdx.y;
   const int64_t col0 = (int64_t)blockIdx.x * TW;
   double2* base = spec + c * g.CS + (int64_t)k0 * g.PS + col0;
-  for (int e = threadIdx.x; e < L * TW; e += NT) {
-    const int i = e / TW, col = e % TW;
-    cpa16(sbuf + e, base + (int64_t)i * nlast + col);
-  }
-  cpa_commit();
-  cpa_wait<0>();
-  __syncthreads();
-  cta_fft<L, TW, NT, INV>(sbuf, TW, 1, tw);
-  for (int e = threadIdx.x; e < L * TW; e += NT) {
-    const int i = e / TW, col = e % TW;
-    base[(int64_t)i * nlast + col] = sbuf[e];
-  }
+  // column col of the tile is sequence col: element i at base + i nlast + col
+  // (TW columns = 128-byte row segments), read by the first stage and written
+  // by the last straight from/to global memory
+  cta_fft_io<L, TW, NT, INV, true, 0, true, true>(sbuf, TW, 1, tw, base, base, 1, nlast);
 }
 
 // ---------------------------------------------------------------------------
@@ -289,7 +281,8 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
     const double w = (k0 == 0 || 2 * k0 == g.n0) ? 1.0 : 2.0;
     // forward: global rows -> (stage 1) -> shared; barrier-separated from the
     // previous row-set's last shared-memory reads by the loop-end barrier
-    cta_fft_io<L, NQ, NT, false, CPAD, true, false>(sbuf, RL, tw, spec + rbase, nullptr, g.CS);
+    cta_fft_io<L, NQ, NT, false, false, CPAD, true, false>(sbuf, 1, RL, tw, spec + rbase, nullptr,
+                                                           g.CS, 1);
     cpa_wait<0>();  // this row-set's Green planes
     __syncthreads();
 #pragma unroll 1
@@ -339,8 +332,8 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
     __syncthreads();  // block solve done: Green planes and r^ rows are free
     if (row + gridDim.x < rows) prefetch_green(row + gridDim.x);
     if (MODE != FM_QUAD)
-      cta_fft_io<L, D, NT, true, CPAD, false, true>(sbuf + ZQ * RL, RL, tw, nullptr,
-                                                    spec + ZQ * g.CS + rbase, g.CS);
+      cta_fft_io<L, D, NT, true, false, CPAD, false, true>(sbuf + ZQ * RL, 1, RL, tw, nullptr,
+                                                           spec + ZQ * g.CS + rbase, g.CS, 1);
     __syncthreads();
   }
   cpa_wait<0>();
