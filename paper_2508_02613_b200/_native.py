@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libjfftb200.so")
+LIB_PATH = os.environ.get("JFFTB_LIB") or os.path.join(HERE, "libjfftb200.so")
 
 OK, EINVAL, ENONFINITE, ECURVATURE, ECUDA = 0, 1, 2, 3, 4
 HOST, DEVICE = 0, 1

@@ -69,19 +69,26 @@ constexpr int nt_for(int butterflies) {
 // inputs stream straight from global in batches, r' goes straight back, and
 // the (up to two) fields are transformed one after the other through one
 // packed smem tile, the s field waiting in registers.
-constexpr int passA_nt(int M) { return nt_for(tw_a(M) * M / 8); }
+// F = 2 holds both packed fields side by side ([k][field][col], 2 TW
+// sequences) and transforms them in one pass: 1024 threads, one CTA per SM.
+constexpr int passA_nt(int M, int F = 1) {
+  return F == 2 ? (2 * tw_a(M) * M / 8 >= 1024 ? 1024 : nt_for(2 * tw_a(M) * M / 8))
+                : nt_for(tw_a(M) * M / 8);
+}
 
 template <int M, int F, int MODE>
-__global__ void __launch_bounds__(passA_nt(M))
+__global__ void __launch_bounds__(passA_nt(M, F))
     passA(FGeom g, const PcgState* __restrict__ st, double* __restrict__ r,
           const double* __restrict__ kp, const double* __restrict__ dinv,
           double2* __restrict__ spec, const double2* __restrict__ tw) {
   constexpr int TW = tw_a(M);
-  constexpr int NT = passA_nt(M);
-  constexpr int RAWN = 2 * M * TW;  // real elements of the tile
+  constexpr int NT = passA_nt(M, F);
+  constexpr int FTW = F * TW;       // sequences of the packed tile
+  constexpr int RAWN = 2 * M * TW;  // real elements of one field's tile
   constexpr int PE = RAWN / NT, CH = PE < 8 ? PE : 8;
   static_assert(PE * NT == RAWN && PE % CH == 0, "pass A tiling");
-  extern __shared__ double2 sbuf[];  // packed tile [k][col], k < M
+  static_assert(F == 1 || MODE != FM_APPLY, "APPLY transforms one field");
+  extern __shared__ double2 sbuf[];  // packed tile [k][field][col], k < M
   if (MODE != FM_APPLY && st->done) return;
   const int c = blockIdx.y;
   const int64_t col0 = (int64_t)blockIdx.x * TW;
@@ -92,7 +99,6 @@ __global__ void __launch_bounds__(passA_nt(M))
   const bool use_k = MODE == FM_ITER;
   const bool use_d = MODE == FM_APPLY ? dc != nullptr : F == 2;
   double* pk = reinterpret_cast<double*>(sbuf);
-  double sv[PE];  // second field (s = D^-1/2 r'), parked in registers
 #pragma unroll
   for (int j0 = 0; j0 < PE; j0 += CH) {
     double a[CH], kv[CH], dv[CH];
@@ -113,37 +119,30 @@ __global__ void __launch_bounds__(passA_nt(M))
         xv = xv - alpha * kv[j];
         rc[(int64_t)i0 * g.PS + col] = xv;
       }
-      const double s = use_d ? dv[j] * xv : xv;
-      sv[j0 + j] = s;
       // packed complex tile: row i0 = 2m + h is Re (h = 0) / Im (h = 1) of z[m]
-      pk[((i0 >> 1) * TW + col) * 2 + (i0 & 1)] = (MODE == FM_APPLY && use_d) ? s : xv;
-    }
-  }
-  constexpr int TWS = kTwN / (2 * M);
-#pragma unroll 1
-  for (int f = 0; f < F; ++f) {
-    if (f == 1) {
-      __syncthreads();  // the first field's unpack has read the tile
-#pragma unroll
-      for (int j = 0; j < PE; ++j) {
-        const int e = threadIdx.x + j * NT;
-        const int i0 = e / TW, col = e % TW;
-        pk[((i0 >> 1) * TW + col) * 2 + (i0 & 1)] = sv[j];
+      double* row = pk + (size_t)(i0 >> 1) * FTW * 2 + (i0 & 1);
+      if (F == 2) {
+        row[col * 2] = xv;
+        row[(TW + col) * 2] = dv[j] * xv;  // s = D^-1/2 r'
+      } else {
+        row[col * 2] = (MODE == FM_APPLY && use_d) ? dv[j] * xv : xv;
       }
     }
-    __syncthreads();
-    cta_fft<M, TW, NT, false>(sbuf, TW, 1, tw);
-    // unpack the packed half-length transform into X[k], k = 0..M
-    double2* out = spec + (f * g.d + c) * g.CS + col0;
-    for (int e = threadIdx.x; e < (M + 1) * TW; e += NT) {
-      const int k = e / TW, q = e % TW;
-      const double2 zk = sbuf[(k % M) * TW + q];
-      const double2 zc = cconj(sbuf[((M - k) % M) * TW + q]);
-      const double2 fe = cscale(cadd(zk, zc), 0.5);
-      const double2 fo = cscale(csub(zk, zc), 0.5);                   // = i Fo
-      const double2 w = __ldg(tw + ((k * TWS) & (kTwN - 1)));         // e^{-2 pi i k / n0}
-      out[(int64_t)k * g.PS + q] = cadd(fe, cmul(w, mul_mi<false>(fo)));  // Fe + w Fo
-    }
+  }
+  __syncthreads();
+  cta_fft<M, FTW, NT, false>(sbuf, FTW, 1, tw);
+  // unpack the packed half-length transforms into X[k], k = 0..M
+  constexpr int TWS = kTwN / (2 * M);
+  for (int e = threadIdx.x; e < (M + 1) * FTW; e += NT) {
+    const int k = e / FTW, q = e % FTW;
+    const int f = q / TW, col = q % TW;
+    const double2 zk = sbuf[(k % M) * FTW + q];
+    const double2 zc = cconj(sbuf[((M - k) % M) * FTW + q]);
+    const double2 fe = cscale(cadd(zk, zc), 0.5);
+    const double2 fo = cscale(csub(zk, zc), 0.5);                   // = i Fo
+    const double2 w = __ldg(tw + ((k * TWS) & (kTwN - 1)));         // e^{-2 pi i k / n0}
+    spec[(f * g.d + c) * g.CS + col0 + (int64_t)k * g.PS + col] =
+        cadd(fe, cmul(w, mul_mi<false>(fo)));                       // Fe + w Fo
   }
 }
 
@@ -469,8 +468,8 @@ template <int M, int F, int MODE>
 void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, const double* kp,
                const double* dinv, double2* spec, const double2* tw) {
   constexpr int TW = tw_a(M);
-  constexpr int NT = passA_nt(M);
-  const size_t smem = sizeof(double2) * TW * M;  // one packed field at a time
+  constexpr int NT = passA_nt(M, F);
+  const size_t smem = sizeof(double2) * F * TW * M;
   auto k = passA<M, F, MODE>;
   static bool attr = false;
   if (!attr) { set_smem(k, smem); attr = true; }
@@ -538,12 +537,13 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
 
 void launchA(const FGeom& g, cudaStream_t s, int F, int mode, const PcgState* st, double* r,
              const double* kp, const double* dinv, double2* spec, const double2* tw) {
-  // one field per launch: two fields in one CTA need either a second 64 KB
-  // tile or the second field parked in registers, and both cost more
-  // occupancy than re-reading r' (3 U) in a second launch saves
-  require(F == 1, "pass A transforms one field per launch");
+  // F = 2 (green-jacobi): r' and s = D^-1/2 r' from one read of r
+  require(F == 1 || (F == 2 && mode != FM_APPLY), "pass A: F = 2 needs INIT / ITER");
   const int n0 = g.n0;
-  if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_ITER>(g, s, st, r, kp, dinv, spec, tw))); }
+  if (F == 2) {
+    if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 2, FM_ITER>(g, s, st, r, kp, dinv, spec, tw))); }
+    else { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 2, FM_INIT>(g, s, st, r, kp, dinv, spec, tw))); }
+  } else if (mode == FM_ITER) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_ITER>(g, s, st, r, kp, dinv, spec, tw))); }
   else if (mode == FM_INIT) { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_INIT>(g, s, st, r, kp, dinv, spec, tw))); }
   else { JF_SIZE_SWITCH(n0, (launchA_M<LL / 2, 1, FM_APPLY>(g, s, st, r, kp, dinv, spec, tw))); }
 }

@@ -231,10 +231,7 @@ static void pcg_precond_phase_fused(jfftb_grid* g, jfftb_jacobi* jac, jfftb_gree
   int scount;
   if (SPECTRAL_PC) {
     // r' = r - alpha Kp and its transform; green-jacobi adds s = D^-1/2 r'
-    fused_stage_A(geo, s, 1, INIT ? FUSED_INIT : FUSED_ITER, B.st, r, B.kp, nullptr, B.spec, tw);
-    if (GJ)
-      fused_stage_A(geo, s, 1, FUSED_APPLY, B.st, r, nullptr, dinv,
-                    B.spec + geo.d * fused_component_stride(geo), tw);
+    fused_stage_A(geo, s, F, INIT ? FUSED_INIT : FUSED_ITER, B.st, r, B.kp, dinv, B.spec, tw);
     if (!INIT) prof_mark(g);
     fused_stage_B(geo, s, false, B.st, B.spec, F * geo.d, tw);
     if (!INIT) prof_mark(g);

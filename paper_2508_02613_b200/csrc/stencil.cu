@@ -89,6 +89,15 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+// predicated form: no branch around the copy (divergent branches around
+// LDGSTS cost the march dozens of issue slots per layer)
+__device__ __forceinline__ void cp_async8_if(void* smem, const void* gmem, bool on) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+      " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(s),
+      "l"(gmem), "r"((int)on));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -119,9 +128,21 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   const bool outp = tx >= 1 && ty >= 1 && gx < n2 && gy < n1;
   const int c2h = wrapi(X0 - 1 + BX3, n2), c1h = wrapi(Y0 - 1 + BY3, n1);
   const int64_t col = (int64_t)c1 * n2 + c2;
-  const bool hx = tx == BX3 - 1, hy = ty == BY3 - 1;
-  const int64_t colx = (int64_t)c1 * n2 + c2h, coly = (int64_t)c1h * n2 + c2,
-                colxy = (int64_t)c1h * n2 + c2h;
+  // halo of a plane: column x = BX3 (BY3 values) and row y = BY3 (BX3 + 1
+  // values) of each component, 3 * 41 copies spread over the first threads
+  constexpr int HPC = BY3 + BX3 + 1;  // halo values per component
+  const int tid = ty * BX3 + tx;
+  const bool h_on = tid < 3 * HPC;
+  int64_t h_src = 0;  // offset from the plane base (component included)
+  int h_dst = 0;      // offset from the slot base, in doubles
+  if (h_on) {
+    const int hc = tid / HPC, e = tid % HPC;
+    const int hy_ = e < BY3 ? e : BY3, hx_ = e < BY3 ? BX3 : e - BY3;
+    h_src = (int64_t)hc * g.N + (int64_t)wrapi(Y0 - 1 + hy_, n1) * n2 + wrapi(X0 - 1 + hx_, n2);
+    h_dst = (hc * (BY3 + 1) + hy_) * (BX3 + 1) + hx_;
+  }
+  (void)c2h;
+  (void)c1h;
 
   double gs[3], fs[3];
 #pragma unroll
@@ -136,15 +157,8 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
     if (!HAS_U) return;
     const double* ub = u + (int64_t)plane_of(kk) * P;
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double* ui = ub + i * g.N;
-      cp_async8(&U[s][i][ty][tx], ui + col);
-      if (hx) {
-        cp_async8(&U[s][i][ty][BX3], ui + colx);
-        if (hy) cp_async8(&U[s][i][BY3][BX3], ui + colxy);
-      }
-      if (hy) cp_async8(&U[s][i][BY3][tx], ui + coly);
-    }
+    for (int i = 0; i < 3; ++i) cp_async8(&U[s][i][ty][tx], ub + i * g.N + col);
+    cp_async8_if(&U[s][0][0][0] + h_dst, ub + h_src, h_on);
   };
   auto fetch_r = [&](int kk, int s) {
     if (rho) cp_async8(&R[s][ty][tx], rho + (int64_t)plane_of(kk) * P + col);
@@ -176,27 +190,20 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   cp_async_commit();
   cp_async_wait<1>();
   __syncthreads();
-  if (HAS_U) {
-    read_corners(s0, uk);
-    // the first layer refills slot s0: every warp must be done reading it
-    __syncthreads();
-  }
 
   double nxt[3] = {0.0, 0.0, 0.0};
   double csum = 0.0;
   int64_t obase = (int64_t)plane_of(k0 - 1) * P + col;  // output index of layer kk
   for (int kk = k0 - 1, j = 0; kk < k1; ++kk, ++j) {
     const int b = j & 1;
-    // slots: s0 = layer kk (u plane kk, rho kk), s1 = kk + 1, s2 = kk + 2
-    if (HAS_U) read_corners(s1, uk1);
+    // slots: s0 = layer kk (u plane kk, rho kk), s1 = kk + 1, s2 = kk + 2.
+    // Both corner planes are read from the ring (no register hand-over
+    // between layers); the slots are refilled after this layer's barrier.
+    if (HAS_U) {
+      read_corners(s0, uk);
+      read_corners(s1, uk1);
+    }
     const double r = rho ? R[s0][ty][tx] : 1.0;
-    // refill: plane kk+3 takes plane kk's slot, rho(kk+2) takes rho(kk-1)'s
-    if (kk + 3 <= k1) fetch_u(kk + 3, s0);
-    if (kk + 2 < k1) fetch_r(kk + 2, s2);
-    cp_async_commit();
-    s0 = s1;
-    s1 = s2;
-    s2 = s2 == 2 ? 0 : s2 + 1;
     double uc[8][3];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -220,8 +227,8 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
       Fy[b][0][i][ty][tx] = f[2][i] + (tx >= 1 ? y0 : 0.0);
       Fy[b][1][i][ty][tx] = f[3][i] + (tx >= 1 ? y1 : 0.0);
     }
-    cp_async_wait<1>();  // plane kk+2 / rho(kk+1) landed (needed next layer)
-    __syncthreads();
+    cp_async_wait<0>();  // plane kk+2 / rho(kk+1) landed (needed next layer)
+    __syncthreads();     // ... and every warp is done reading slot s0
     if (ty >= 1) {
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
@@ -237,10 +244,13 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
     }
     obase += P;
     if (obase >= g.N) obase -= g.N;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) uk[q][i] = uk1[q][i];
+    // refill: plane kk+3 takes plane kk's slot, rho(kk+2) takes rho(kk-1)'s
+    if (kk + 3 <= k1) fetch_u(kk + 3, s0);
+    if (kk + 2 < k1) fetch_r(kk + 2, s2);
+    cp_async_commit();
+    s0 = s1;
+    s1 = s2;
+    s2 = s2 == 2 ? 0 : s2 + 1;
   }
   cp_async_wait<0>();
   if (MODE == VOX_K && partials) {
