@@ -289,11 +289,14 @@ def run_ours(args, rank, world):
     peak, peak_src = peak_hbm()
     per_iter_ms = ms_total / iters_total
     alg_iter = R.algorithmic_bytes(args.kind, d, Nn)
+    # power-of-two grids run the fused FFT passes (fused.cu) unless disabled
+    fused_path = (all(k & (k - 1) == 0 and 16 <= k <= 2048 for k in shape)
+                  and os.environ.get("JFFTB_DISABLE_FUSED") != "1")
     stages = {}
     for k, nm in enumerate(R.STAGES):
         if prof_iters:
             avg = stage_ms[k] / prof_iters
-            b = R.kernel_bytes(nm, args.kind, d, Nn)
+            b = R.kernel_bytes(nm, args.kind, d, Nn, fused=fused_path)
             stages[nm] = {"ms": avg, "share": stage_ms[k] / max(stage_ms.sum(), 1e-30),
                           "alg_bytes": b, "GBps": (b / (avg / 1e3) / 1e9) if avg > 0 and b else None}
     ours = {k: v for k, v in stages.items() if not k.startswith("fft")}

@@ -24,14 +24,24 @@ def algorithmic_bytes(kind: str, d: int, n_nodes: int) -> int:
     return PER_ITER_U[kind](d) * 8 * int(n_nodes)
 
 
-def kernel_bytes(stage: str, kind: str, d: int, n_nodes: int) -> int:
+def kernel_bytes(stage: str, kind: str, d: int, n_nodes: int, fused: bool = True) -> int:
     """Compulsory bytes of one launch of a stage of this build's iteration
-    (stored Green blocks: d = 2 -> 4, d = 3 -> 9 doubles per frequency)."""
+    (stored Green blocks: d = 2 -> 4, d = 3 -> 9 doubles per frequency).
+
+    ``fused`` = the fused-FFT path of power-of-two grids (fused.cu), where
+    "update" is pass A (r' = r - alpha Kp and the axis-0 transforms), the
+    FFT stages are passes B / B', "spectral" is pass C and "pupdate" is pass I
+    (which also carries the lagged x += alpha p)."""
     U = 8 * int(n_nodes)
     gj = kind == "green-jacobi"
     green_planes = 4 if d == 2 else 9
     if stage == "stencil":
         return (2 * d + 1) * U                       # p, rho -> Kp
+    if fused and kind in ("green", "green-jacobi"):
+        if stage == "update":                        # r, Kp (, D) -> r', spectra
+            return (6 * d if gj else 4 * d) * U
+        if stage == "pupdate":                       # z^, (D), p, x -> p, x
+            return (6 * d if gj else 5 * d) * U
     if stage == "update":
         extra = d if gj else (d if kind == "jacobi" else 0)
         dinv = d if kind in ("jacobi", "green-jacobi") else 0
