@@ -290,7 +290,7 @@ def run_ours(args, rank, world):
     per_iter_ms = ms_total / iters_total
     alg_iter = R.algorithmic_bytes(args.kind, d, Nn)
     # power-of-two grids run the fused FFT passes (fused.cu) unless disabled
-    fused_path = (all(k & (k - 1) == 0 and 16 <= k <= 2048 for k in shape)
+    fused_path = (all(k & (k - 1) == 0 and 16 <= k <= 2048 for k in P["gh"].shape)
                   and os.environ.get("JFFTB_DISABLE_FUSED") != "1")
     stages = {}
     for k, nm in enumerate(R.STAGES):
