@@ -229,7 +229,7 @@ constexpr int CPAD = 8;  // one padding slot every 8 elements of a row
 // Green planes staged in smem (GSTAGE) or read straight from global in the solve
 constexpr bool kGStage = true;
 constexpr int passC_gp(int D) { return kGStage ? (D == 2 ? 4 : 9) : 0; }
-constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / 8); }
+constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / 16); }
 constexpr int passC_bufd(int D, int L, int F) {
   return F * D * padded_len<CPAD>(L) * 2 + passC_gp(D) * L;
 }
@@ -285,7 +285,8 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
     cpa_wait<0>();  // this row-set's Green planes
     __syncthreads();
 #pragma unroll 1
-    auto green_block = [&](int k) {
+    for (int k = threadIdx.x; k < L; k += NT) {
+      const int64_t f = rbase + k;
       HB<D> B;
       if constexpr (kGStage) {
 #pragma unroll
@@ -296,39 +297,30 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
           B.im[o] = gsm[(D + 2 * o + 1) * L + k];
         }
       } else {
-        B = ld_block<D>(gpc, Nh, rbase + k);
+        B = ld_block<D>(gpc, Nh, f);
       }
-      return B;
-    };
-    // two sweeps over the row (fewer live registers than one fused sweep):
-    // q_r = r^H Gt r of the r^ rows (green-jacobi), then z^ = G s^ / N and
-    // q_s = s^H G s over the solved rows
-    if (F == 2 && MODE != FM_QUAD && MODE != FM_APPLY) {
-#pragma unroll 1
-      for (int k = threadIdx.x; k < L; k += NT) {
-        double2 rr[D], tmp[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) rr[a] = sbuf[a * RL + pidx<CPAD>(k)];
-        q0 += w * hb_apply<D>(gterm == gpc ? green_block(k) : ld_block<D>(gterm, Nh, rbase + k),
-                              rr, tmp);
-      }
-    }
-#pragma unroll 1
-    for (int k = threadIdx.x; k < L; k += NT) {
       double2 s[D], z[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) s[a] = sbuf[(ZQ + a) * RL + pidx<CPAD>(k)];
-      const double qs = hb_apply<D>(green_block(k), s, z);
+      const double qs = hb_apply<D>(B, s, z);
       if (MODE == FM_QUAD) {
         q0 += w * qs;  // gpc is the termination operator here
       } else if (MODE != FM_APPLY) {
-        q1 += w * qs;
-        if (F == 1) {
+        if (F == 2) {
+          double2 rr[D], tmp[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) rr[a] = sbuf[a * RL + pidx<CPAD>(k)];
+          const double qr = (gterm == gpc) ? hb_apply<D>(B, rr, tmp)
+                                           : hb_apply<D>(ld_block<D>(gterm, Nh, f), rr, tmp);
+          q0 += w * qr;
+          q1 += w * qs;
+        } else {
+          q1 += w * qs;
           if (gterm == gpc) {
             q0 += w * qs;
           } else {
             double2 tmp[D];
-            q0 += w * hb_apply<D>(ld_block<D>(gterm, Nh, rbase + k), s, tmp);
+            q0 += w * hb_apply<D>(ld_block<D>(gterm, Nh, f), s, tmp);
           }
         }
       }
