@@ -263,14 +263,20 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
   double q0 = 0.0, q1 = 0.0;
   constexpr int ZQ = F == 2 ? D : 0;  // first row of the solved spectrum
   double* gsm = reinterpret_cast<double*>(sbuf + NQ * RL);
+  // the Green planes of a row-set (GP contiguous L-double runs) arrive by
+  // bulk copies issued by one thread and complete on gbar
+  __shared__ uint64_t gbar;
+  unsigned gphase = 0;
+  if (kGStage && threadIdx.x == 0) mbar_init(&gbar, 1);
+  __syncthreads();
   auto prefetch_green = [&](int64_t row) {
-    if (!kGStage) return;
+    if (!kGStage || threadIdx.x != 0) return;
     const int64_t rbase = row * L;
-    for (int e = threadIdx.x; e < GP * L / 2; e += NT) {  // 16-byte pairs
-      const int p = (2 * e) / L, k = (2 * e) % L;
-      cpa16(gsm + 2 * e, gpc + p * Nh + rbase + k);
-    }
-    cpa_commit();
+    fence_proxy_async();  // the previous row-set's reads of gsm come first
+    mbar_expect_tx(&gbar, GP * L * sizeof(double));
+#pragma unroll 1
+    for (int p = 0; p < GP; ++p)
+      bulk_g2s(gsm + p * L, gpc + p * Nh + rbase, L * sizeof(double), &gbar);
   };
   int64_t row = blockIdx.x;
   if (row < rows) prefetch_green(row);
@@ -282,7 +288,8 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
     // previous row-set's last shared-memory reads by the loop-end barrier
     cta_fft_io<L, NQ, NT, false, false, CPAD, true, false>(sbuf, 1, RL, tw, spec + rbase, nullptr,
                                                            g.CS, 1);
-    cpa_wait<0>();  // this row-set's Green planes
+    if (kGStage) mbar_wait(&gbar, gphase);  // this row-set's Green planes
+    gphase ^= 1;
     __syncthreads();
 #pragma unroll 1
     for (int k = threadIdx.x; k < L; k += NT) {
@@ -335,7 +342,6 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
                                                            spec + ZQ * g.CS + rbase, g.CS, 1);
     __syncthreads();
   }
-  cpa_wait<0>();
   if (MODE != FM_APPLY) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     q0 = warp_sum(q0 * invN);
