@@ -333,7 +333,9 @@ void pcg_dispatch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_gr
 bool fused_supported(const Geom& g);
 int64_t fused_spec_elems(const Geom& g);   // complex elements per spectral component
 constexpr int kFusedMaxBlocks = 148 * 4 * 8;  // bound on pass-C partial pairs
-constexpr int kTwiddleN = 4096;               // twiddle table entries (fft.cuh kTwN)
+// twiddle table: 4096 entries of exp(-2 pi i j / 4096), then per-stage tables
+// (fft.cuh kTwN, tw_stage_off): 13 spans x 3 radices x 4096
+constexpr int kTwiddleN = 4096 + 13 * 3 * 4096;
 // complex elements per spectral component of whichever layout the grid uses
 inline int64_t spec_elems(const jfftb_grid* g) {
   return g->fused ? fused_spec_elems(g->geo) : g->geo.Nh;

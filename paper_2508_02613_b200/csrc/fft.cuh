@@ -5,8 +5,9 @@
 // buf[q * qs + k * ks], with a Stockham autosort radix-8 (+ one radix-2/4)
 // schedule.  Every stage reads all its butterfly inputs into registers,
 // barriers, and writes in place, so no ping-pong buffer is needed; NT threads
-// share the NSEQ * L / R butterflies of a stage.  Twiddles come from one
-// 4096-entry table of exp(-2 pi i j / 4096) (fp64, built once per grid).
+// share the NSEQ * L / R butterflies of a stage.  Twiddles come from
+// per-stage tables copied out of one 4096-entry table of exp(-2 pi i j / 4096)
+// (fp64, built once per grid), laid out so a warp's reads are contiguous.
 // Forward = numpy's unnormalised exp(-i...) convention; INV = exp(+i...)
 // without the 1/L factor (folded into the spectral multiply).
 #pragma once
@@ -16,6 +17,17 @@
 namespace jfftb {
 
 constexpr int kTwN = 4096;
+
+// Per-stage twiddle tables follow the 4096-entry table: the stage of span
+// P = NS * R (radix R) reads w_P^(j t) for j < NS, t = 1..R-1 at
+// [(t - 1) * NS + j], so the threads of a warp (consecutive j) read
+// consecutive entries -- a strided walk through the 4096 table would touch
+// one cache line per thread in the late stages.  Same values, bit for bit.
+__host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
+__host__ __device__ constexpr int tw_ridx(int R) { return R == 8 ? 0 : (R == 4 ? 1 : 2); }
+__host__ __device__ constexpr int tw_stage_off(int P, int R) {
+  return 4096 + (ilog2c(P) * 3 + tw_ridx(R)) * 4096;
+}
 
 // Ampere+ asynchronous global -> shared copies (LDGSTS), used to prefetch the
 // next tile while the current one is transformed
@@ -187,11 +199,12 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
     double2 v[PER][8];
     int qq[PER], jj[PER];
     double2 ws[SHARE ? 8 : 1];
+    const double2* __restrict__ tws = tw + tw_stage_off(NS * R, R);
     if constexpr (SHARE) {
       if (NS > 1) {
-        const int base = ((tid % NB) % NS) * (kTwN / (NS * R));
+        const int jb = (tid % NB) % NS;
 #pragma unroll
-        for (int t = 1; t < R; ++t) ws[SHARE ? t : 0] = __ldg(tw + ((base * t) & (kTwN - 1)));
+        for (int t = 1; t < R; ++t) ws[SHARE ? t : 0] = __ldg(tws + (t - 1) * NS + jb);
       }
     }
 #pragma unroll
@@ -210,10 +223,10 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
           for (int t = 0; t < R; ++t) v[m][t] = src[pidx<PAD>(jj[m] + t * NB) * ks];
         }
         if (NS > 1) {
-          const int base = (jj[m] % NS) * (kTwN / (NS * R));
+          const int jb = jj[m] % NS;
 #pragma unroll
           for (int t = 1; t < R; ++t) {
-            const double2 w = SHARE ? ws[SHARE ? t : 0] : __ldg(tw + ((base * t) & (kTwN - 1)));
+            const double2 w = SHARE ? ws[SHARE ? t : 0] : __ldg(tws + (t - 1) * NS + jb);
             v[m][t] = INV ? cmulc(v[m][t], w) : cmul(v[m][t], w);
           }
         }

@@ -20,6 +20,8 @@
 #include "common.cuh"
 #include "fft.cuh"
 
+#include <cstdlib>
+
 namespace jfftb {
 
 namespace {
@@ -37,6 +39,17 @@ __global__ void twiddle_kernel(double2* tw) {
     sincospi(-2.0 * (double)j / (double)kTwN, &s, &c);
     tw[j] = make_double2(c, s);
   }
+}
+// per-stage tables (fft.cuh tw_stage_off), copied from the 4096 table
+__global__ void twiddle_stage_kernel(double2* tw) {
+  const int lgP = blockIdx.y, ri = blockIdx.z;
+  const int P = 1 << lgP, R = ri == 0 ? 8 : (ri == 1 ? 4 : 2);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (P < R || P > kTwN) return;
+  const int NS = P / R;
+  if (e >= (R - 1) * NS) return;
+  const int t = e / NS + 1, j = e % NS;
+  tw[tw_stage_off(P, R) + e] = tw[(j * (kTwN / P) * t) & (kTwN - 1)];
 }
 
 enum FMode { FM_APPLY = FUSED_APPLY, FM_INIT = FUSED_INIT, FM_ITER = FUSED_ITER, FM_QUAD = 3 };
@@ -592,6 +605,8 @@ void launchI(const FGeom& g, cudaStream_t s, int mode, const PcgState* st, const
 
 void launch_twiddles(cudaStream_t s, double2* tw) {
   twiddle_kernel<<<kTwN / 256, 256, 0, s>>>(tw);
+  JF_LAUNCHED();
+  twiddle_stage_kernel<<<dim3(kTwN / 256, 13, 3), 256, 0, s>>>(tw);
   JF_LAUNCHED();
 }
 
