@@ -84,18 +84,16 @@ constexpr int nt_for(int butterflies) {
 // packed smem tile, the s field waiting in registers.
 // F = 2 holds both packed fields side by side ([k][field][col], 2 TW
 // sequences) and transforms them in one pass: 1024 threads, one CTA per SM.
-constexpr int passA_nt(int M, int F = 1) {
-  return F == 2 ? (2 * tw_a(M) * M / 8 >= 1024 ? 1024 : nt_for(2 * tw_a(M) * M / 8))
-                : nt_for(tw_a(M) * M / 8);
+constexpr int passA_nt(int M, int F, int TW) {
+  return F == 2 ? (2 * TW * M / 8 >= 1024 ? 1024 : nt_for(2 * TW * M / 8)) : nt_for(TW * M / 8);
 }
 
-template <int M, int F, int MODE>
-__global__ void __launch_bounds__(passA_nt(M, F))
+template <int M, int F, int MODE, int TW>
+__global__ void __launch_bounds__(passA_nt(M, F, TW), passA_nt(M, F, TW) <= 512 ? 2 : 1)
     passA(FGeom g, const PcgState* __restrict__ st, double* __restrict__ r,
           const double* __restrict__ kp, const double* __restrict__ dinv,
           double2* __restrict__ spec, const double2* __restrict__ tw) {
-  constexpr int TW = tw_a(M);
-  constexpr int NT = passA_nt(M, F);
+  constexpr int NT = passA_nt(M, F, TW);
   constexpr int FTW = F * TW;       // sequences of the packed tile
   constexpr int RAWN = 2 * M * TW;  // real elements of one field's tile
   constexpr int PE = RAWN / NT, CH = PE < 8 ? PE : 8;
@@ -109,9 +107,9 @@ __global__ void __launch_bounds__(passA_nt(M, F))
   double* rc = r + c * g.N + col0;
   const double* kc = kp ? kp + c * g.N + col0 : nullptr;
   const double* dc = dinv ? dinv + c * g.N + col0 : nullptr;
+  double* pk = reinterpret_cast<double*>(sbuf);
   const bool use_k = MODE == FM_ITER;
   const bool use_d = MODE == FM_APPLY ? dc != nullptr : F == 2;
-  double* pk = reinterpret_cast<double*>(sbuf);
 #pragma unroll
   for (int j0 = 0; j0 < PE; j0 += CH) {
     double a[CH], kv[CH], dv[CH];
@@ -144,18 +142,25 @@ __global__ void __launch_bounds__(passA_nt(M, F))
   }
   __syncthreads();
   cta_fft<M, FTW, NT, false>(sbuf, FTW, 1, tw);
-  // unpack the packed half-length transforms into X[k], k = 0..M
+  // unpack the packed half-length transforms into X[k], k = 0..M, pairwise:
+  // X[k] and X[M-k] come from the same two entries z[k], z[M-k] (k = 0
+  // pairs with the Nyquist row M), so each entry is read once
   constexpr int TWS = kTwN / (2 * M);
-  for (int e = threadIdx.x; e < (M + 1) * FTW; e += NT) {
-    const int k = e / FTW, q = e % FTW;
-    const int f = q / TW, col = q % TW;
-    const double2 zk = sbuf[(k % M) * FTW + q];
-    const double2 zc = cconj(sbuf[((M - k) % M) * FTW + q]);
+  auto unpack = [&](double2 zk, double2 zc, int k) {
     const double2 fe = cscale(cadd(zk, zc), 0.5);
     const double2 fo = cscale(csub(zk, zc), 0.5);                   // = i Fo
     const double2 w = __ldg(tw + ((k * TWS) & (kTwN - 1)));         // e^{-2 pi i k / n0}
-    spec[(f * g.d + c) * g.CS + col0 + (int64_t)k * g.PS + col] =
-        cadd(fe, cmul(w, mul_mi<false>(fo)));                       // Fe + w Fo
+    return cadd(fe, cmul(w, mul_mi<false>(fo)));                    // Fe + w Fo
+  };
+  for (int e = threadIdx.x; e < (M / 2 + 1) * FTW; e += NT) {
+    const int k = e / FTW, q = e % FTW;
+    const int f = q / TW, col = q % TW;
+    const int kc = M - k;
+    const double2 za = sbuf[k * FTW + q];
+    const double2 zb = sbuf[(kc % M) * FTW + q];
+    double2* out = spec + (f * g.d + c) * g.CS + col0 + col;
+    out[(int64_t)k * g.PS] = unpack(za, cconj(zb), k);
+    if (kc != k) out[(int64_t)kc * g.PS] = unpack(zb, cconj(za), kc);
   }
 }
 
@@ -239,31 +244,33 @@ __device__ __forceinline__ double hb_apply(const HB<D>& B, const double2 (&s)[D]
 // transform instead of four.  The Green planes of the next row-set are copied
 // to shared memory with cp.async while the current inverse transform runs.
 constexpr int CPAD = 8;  // one padding slot every 8 elements of a row
-// Green planes staged in smem (GSTAGE) or read straight from global in the solve
+// Green planes staged in smem (GS) or read straight from global in the solve
+// (measured at 512^3: staged 3.69 ms, direct 4.19 ms)
 constexpr bool kGStage = true;
-constexpr int passC_gp(int D) { return kGStage ? (D == 2 ? 4 : 9) : 0; }
+constexpr int passC_gp(int D, bool GS) { return GS ? (D == 2 ? 4 : 9) : 0; }
 constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / 16); }
-constexpr int passC_bufd(int D, int L, int F) {
-  return F * D * padded_len<CPAD>(L) * 2 + passC_gp(D) * L;
+constexpr int passC_bufd(int D, int L, int F, bool GS = true) {
+  return F * D * padded_len<CPAD>(L) * 2 + passC_gp(D, GS) * L;
 }
 // resident CTAs per SM the launch bounds aim for (capped by shared memory).
 // Double buffering the rows (next row-set in flight during this one's
 // transforms) was measured slower at 512^3 (6.6 ms vs 5.7 ms): it halves the
 // resident CTAs.
-constexpr int passC_minb(int D, int L, int F) {
-  return passC_bufd(D, L, F) * 8 <= 72 * 1024 ? 3 : (passC_bufd(D, L, F) * 8 <= 110 * 1024 ? 2 : 1);
+constexpr int passC_minb(int D, int L, int F, bool GS = true) {
+  return passC_bufd(D, L, F, GS) * 8 <= 72 * 1024 ? 3
+                                                   : (passC_bufd(D, L, F, GS) * 8 <= 110 * 1024 ? 2 : 1);
 }
 
-template <int D, int L, int F, int MODE>
-__global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
+template <int D, int L, int F, int MODE, bool GS>
+__global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     passC(FGeom g, const PcgState* __restrict__ st, const double* __restrict__ gpc,
           const double* __restrict__ gterm, double2* __restrict__ spec,
           double* __restrict__ partials, const double2* __restrict__ tw) {
   constexpr int NQ = F * D;  // rows held per frequency row
   constexpr int NT = passC_nt(D, L, F);
   constexpr int RL = padded_len<CPAD>(L);
-  constexpr int GP = passC_gp(D);            // Green planes staged with the rows
-  constexpr int BUFD = passC_bufd(D, L, F);  // doubles of shared memory
+  constexpr int GP = passC_gp(D, GS);            // Green planes staged with the rows
+  constexpr int BUFD = passC_bufd(D, L, F, GS);  // doubles of shared memory
   static_assert(BUFD == NQ * RL * 2 + GP * L, "buffer layout");
   // [ rows: NQ x RL double2 | Green planes: GP x L double ]
   extern __shared__ double2 sbuf[];
@@ -280,10 +287,10 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
   // bulk copies issued by one thread and complete on gbar
   __shared__ uint64_t gbar;
   unsigned gphase = 0;
-  if (kGStage && threadIdx.x == 0) mbar_init(&gbar, 1);
+  if (GS && threadIdx.x == 0) mbar_init(&gbar, 1);
   __syncthreads();
   auto prefetch_green = [&](int64_t row) {
-    if (!kGStage || threadIdx.x != 0) return;
+    if (!GS || threadIdx.x != 0) return;
     const int64_t rbase = row * L;
     fence_proxy_async();  // the previous row-set's reads of gsm come first
     mbar_expect_tx(&gbar, GP * L * sizeof(double));
@@ -301,14 +308,14 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F))
     // previous row-set's last shared-memory reads by the loop-end barrier
     cta_fft_io<L, NQ, NT, false, false, CPAD, true, false>(sbuf, 1, RL, tw, spec + rbase, nullptr,
                                                            g.CS, 1);
-    if (kGStage) mbar_wait(&gbar, gphase);  // this row-set's Green planes
+    if (GS) mbar_wait(&gbar, gphase);  // this row-set's Green planes
     gphase ^= 1;
     __syncthreads();
 #pragma unroll 1
     for (int k = threadIdx.x; k < L; k += NT) {
       const int64_t f = rbase + k;
       HB<D> B;
-      if constexpr (kGStage) {
+      if constexpr (GS) {
 #pragma unroll
         for (int a = 0; a < D; ++a) B.dg[a] = gsm[a * L + k];
 #pragma unroll
@@ -483,18 +490,22 @@ FGeom fgeom(const Geom& g) {
 }
 
 // ---- size dispatch -------------------------------------------------------
-template <int M, int F, int MODE>
-void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, const double* kp,
-               const double* dinv, double2* spec, const double2* tw) {
-  constexpr int TW = tw_a(M);
-  constexpr int NT = passA_nt(M, F);
+template <int M, int F, int MODE, int TW>
+void launchA_MT(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, const double* kp,
+                const double* dinv, double2* spec, const double2* tw) {
+  constexpr int NT = passA_nt(M, F, TW);
   const size_t smem = sizeof(double2) * F * TW * M;
-  auto k = passA<M, F, MODE>;
+  auto k = passA<M, F, MODE, TW>;
   static bool attr = false;
   if (!attr) { set_smem(k, smem); attr = true; }
   dim3 grid((unsigned)(g.PS / TW), g.d);
   k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
   JF_LAUNCHED();
+}
+template <int M, int F, int MODE>
+void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, const double* kp,
+               const double* dinv, double2* spec, const double2* tw) {
+  launchA_MT<M, F, MODE, tw_a(M)>(g, s, st, r, kp, dinv, spec, tw);
 }
 template <int L, bool INV, bool PRED>
 void launchB_L(const FGeom& g, cudaStream_t s, const PcgState* st, double2* spec, int comp0,
@@ -513,9 +524,9 @@ template <int D, int L, int F, int MODE>
 int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* gpc,
               const double* gterm, double2* spec, double* partials, const double2* tw) {
   constexpr int NT = passC_nt(D, L, F);
-  constexpr int BUFD = passC_bufd(D, L, F);
+  constexpr int BUFD = passC_bufd(D, L, F, kGStage);
   const size_t smem = sizeof(double) * BUFD;
-  auto k = passC<D, L, F, MODE>;
+  auto k = passC<D, L, F, MODE, kGStage>;
   static int per_sm = -1;  // per instantiation
   if (per_sm < 0) {
     set_smem(k, smem);
