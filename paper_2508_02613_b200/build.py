@@ -17,7 +17,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libjfftb200.so")
-SOURCES = ["api.cu", "stencil.cu", "blas.cu", "spectral.cu", "pcg.cu", "fused.cu"]
+SOURCES = ["api.cu", "stencil.cu", "blas.cu", "spectral.cu", "pcg.cu", "fused.cu", "hostio.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", os.path.join(CUDA_HOME, "lib64"),
-           "-lcufft", "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
+           "-lcufft", "-lpthread", "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -72,8 +72,7 @@ const double* stage_in(jfftb_grid* g, const double* src, size_t count, int where
   if (where == JFFTB_DEVICE) return src;
   require(where == JFFTB_HOST, "where must be JFFTB_HOST or JFFTB_DEVICE");
   tmp.reset(count * sizeof(double));
-  JF_CUDA(cudaMemcpyAsync(tmp.ptr, src, count * sizeof(double), cudaMemcpyHostToDevice,
-                          g->stream));
+  copy_h2d(g, tmp.ptr, src, count * sizeof(double), g->stream);
   return tmp.as<double>();
 }
 double* stage_out(double* dst, size_t count, int where, DevBuf& tmp) {
@@ -84,10 +83,7 @@ double* stage_out(double* dst, size_t count, int where, DevBuf& tmp) {
   return tmp.as<double>();
 }
 void finish_out(jfftb_grid* g, double* dst, const double* dev, size_t count, int where) {
-  if (where == JFFTB_HOST) {
-    JF_CUDA(cudaMemcpyAsync(dst, dev, count * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
-    JF_CUDA(cudaStreamSynchronize(g->stream));
-  }
+  if (where == JFFTB_HOST) copy_d2h(g, dst, dev, count * sizeof(double), g->stream);
 }
 
 double* ensure_partials(jfftb_grid* g, int count) {
@@ -412,6 +408,7 @@ void grid_free(jfftb_grid* g) {
     if (g->ws) cudaFree(g->ws);
     if (g->ws_host) cudaFreeHost(g->ws_host);
     if (g->twiddle) cudaFree(g->twiddle);
+    free_host_staging(g);
     prof_collect(g, 0, true);
     for (auto e : g->ev_free) cudaEventDestroy(e);
     cudaStreamDestroy(g->own_stream);
@@ -852,11 +849,13 @@ int jfftb_jacobi_export(jfftb_jacobi* jac, double* out, int where) {
     DeviceGuard dg(g->device);
     const int64_t n = g->geo.d * g->geo.N;
     require(out != nullptr, "null output");
-    JF_CUDA(cudaMemcpyAsync(out, jac->inv_sqrt, sizeof(double) * n,
-                            where == JFFTB_HOST ? cudaMemcpyDeviceToHost
-                                                : cudaMemcpyDeviceToDevice,
-                            g->stream));
-    JF_CUDA(cudaStreamSynchronize(g->stream));
+    if (where == JFFTB_HOST) {
+      copy_d2h(g, out, jac->inv_sqrt, sizeof(double) * n, g->stream);
+    } else {
+      JF_CUDA(cudaMemcpyAsync(out, jac->inv_sqrt, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                              g->stream));
+      JF_CUDA(cudaStreamSynchronize(g->stream));
+    }
   });
 }
 
@@ -912,10 +911,10 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     *hs = h0;
     JF_CUDA(cudaMemcpyAsync(B.st, hs, sizeof(PcgState), cudaMemcpyHostToDevice, s));
     JF_CUDA(cudaMemsetAsync(B.x, 0, sizeof(double) * n, s));
-    JF_CUDA(cudaMemcpyAsync(B.rs, rhs, sizeof(double) * n,
-                            where == JFFTB_HOST ? cudaMemcpyHostToDevice
-                                                : cudaMemcpyDeviceToDevice,
-                            s));
+    if (where == JFFTB_HOST)
+      copy_h2d(g, B.rs, rhs, sizeof(double) * n, s);
+    else
+      JF_CUDA(cudaMemcpyAsync(B.rs, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     auto poll = [&]() {
       JF_CUDA(cudaMemcpyAsync(hs, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       JF_CUDA(cudaStreamSynchronize(s));
@@ -949,10 +948,10 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     *terminated = (hs->gnorm2 <= eta) ? JFFTB_CONVERGED : JFFTB_ITERATION_CAP;
     launch_sub_mean(geo, s, B.x, ensure_partials(g, kRedBlocks * 3 + 3));
     if (x_out) {
-      JF_CUDA(cudaMemcpyAsync(x_out, B.x, sizeof(double) * n,
-                              where == JFFTB_HOST ? cudaMemcpyDeviceToHost
-                                                  : cudaMemcpyDeviceToDevice,
-                              s));
+      if (where == JFFTB_HOST)
+        copy_d2h(g, x_out, B.x, sizeof(double) * n, s);
+      else
+        JF_CUDA(cudaMemcpyAsync(x_out, B.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     }
     JF_CUDA(cudaStreamSynchronize(s));
     if (wall_s)

@@ -88,6 +88,7 @@ struct jfftb_grid {
   cufftHandle plan_fwd_d = 0, plan_inv_d = 0, plan_fwd_2d = 0;
   bool plans_ready = false;
   void* fft_work = nullptr;
+  void* host_stage = nullptr;   // pinned staging ring for pageable host copies (hostio.cu)
   size_t fft_work_bytes = 0;
   // reduction scratch
   double* partials = nullptr;   // per-block partial sums
@@ -292,6 +293,12 @@ void launch_total_strain(const Geom& g, cudaStream_t s, const double* u,
 // per-block partials of sum_Q rho C0 (E + B u), M values per block
 int launch_stress_sum(const Geom& g, cudaStream_t s, const double* u, const double* rho,
                       double lam, double mu, const double* ebar, double* partials);
+
+// host <-> device field copies (hostio.cu): pageable host memory is staged
+// through a pinned ring by a team of host threads; d2h returns synchronised
+void copy_h2d(jfftb_grid* g, void* dst, const void* src, size_t bytes, cudaStream_t s);
+void copy_d2h(jfftb_grid* g, void* dst, const void* src, size_t bytes, cudaStream_t s);
+void free_host_staging(jfftb_grid* g);
 
 // vector algebra
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic

@@ -67,3 +67,43 @@ def test_handles_may_be_destroyed_in_any_order():
     for h in (op, green, jac):
         assert getattr(lib, h._destroy)(h.ptr) == N.OK
         h.ptr = None
+
+
+def test_host_copies_match_device_resident(problem):
+    """Pageable host arrays go through the pinned staging ring (hostio.cu):
+    48 MiB fields span two 32 MiB chunks plus a ragged tail.  The solution
+    returned into a fresh pageable array, into a pinned array (direct DMA)
+    and into device memory must agree bit for bit, and so must the operator
+    applied to host and to device arrays."""
+    import torch
+    grid, op, green, u = problem
+    from paper_2508_02613_b200.operators import op_handle
+    from paper_2508_02613_b200.solver import pcg_device
+    rhs = assemble_rhs(op, np.array([0.0, 0.0, 0.0, 0.0, 0.0, np.sqrt(0.5)]))
+    pc = build_preconditioner("green-jacobi", op, green)
+    rep = pcg(op, rhs, pc, green, eta=-1.0, max_iter=12)  # pageable in and out
+    dev = torch.device("cuda", N.device_id())
+    rhs_d = torch.from_numpy(np.ascontiguousarray(rhs.values)).to(dev)
+    x_d = torch.empty_like(rhs_d)
+    torch.cuda.synchronize()
+    it, hist, _, _ = pcg_device(op_handle(op), "green-jacobi", green.handle, pc.jacobi.handle,
+                                rhs_d.data_ptr(), x_d.data_ptr(), -1.0, 12)
+    assert it == rep.iterations and hist == rep.residual_history
+    assert np.array_equal(x_d.cpu().numpy(), rep.solution.values)
+    # pinned input and output: the direct path
+    lib = N.load()
+    xin = torch.from_numpy(np.ascontiguousarray(u.values)).pin_memory()
+    xout = torch.empty_like(xin).pin_memory()
+    N.check(lib.jfftb_apply_system(op_handle(op).ptr, N.vptr(xin.numpy()), N.vptr(xout.numpy()),
+                                   N.HOST))
+    assert np.array_equal(xout.numpy(), apply_system(op, u).values)
+    out_d = torch.empty_like(rhs_d)
+    u_d = xin.to(dev)
+    torch.cuda.synchronize()
+    N.check(lib.jfftb_apply_system(op_handle(op).ptr, C_ptr(u_d), C_ptr(out_d), N.DEVICE))
+    assert np.array_equal(out_d.cpu().numpy(), xout.numpy())
+
+
+def C_ptr(t):
+    import ctypes
+    return ctypes.c_void_p(t.data_ptr())
