@@ -22,8 +22,14 @@ namespace {
 
 // 3-D tile (threads), emits 31 x 7 columns (32 x 16 measured slower: 4.05 vs
 // 3.80 ms at 512^3 -- one CTA of 16 warps hides less than two of 8)
-constexpr int BX3 = 32, BY3 = 8;
-constexpr int MINB3 = BY3 <= 8 ? 2 : 1;  // resident CTAs per SM the launch bounds target
+#ifndef JF_ST_BY
+#define JF_ST_BY 8
+#endif
+#ifndef JF_ST_MINB
+#define JF_ST_MINB 2
+#endif
+constexpr int BX3 = 32, BY3 = JF_ST_BY;
+constexpr int MINB3 = BY3 <= 8 ? JF_ST_MINB : 1;  // resident CTAs per SM the launch bounds target
 constexpr int BX2 = 128;           // 2-D tile, emits 127 columns
 
 __device__ __forceinline__ int wrapi(int i, int n) {
@@ -224,8 +230,15 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
       const double y1 = __shfl_up_sync(0xffffffffu, f[7][i], 1);
       ak[i] = nxt[i] + f[0][i] + x0;
       nxt[i] = f[1][i] + x1;
+#ifndef JF_ST_SEL
+      // lane 0 is a halo column: whatever it hands over only reaches other
+      // halo columns (never an output node), so no select is needed
+      Fy[b][0][i][ty][tx] = f[2][i] + y0;
+      Fy[b][1][i][ty][tx] = f[3][i] + y1;
+#else
       Fy[b][0][i][ty][tx] = f[2][i] + (tx >= 1 ? y0 : 0.0);
       Fy[b][1][i][ty][tx] = f[3][i] + (tx >= 1 ? y1 : 0.0);
+#endif
     }
     cp_async_wait<0>();  // plane kk+2 / rho(kk+1) landed (needed next layer)
     __syncthreads();     // ... and every warp is done reading slot s0
