@@ -77,6 +77,25 @@ int jfftb_grid_destroy(jfftb_grid* g);
 int jfftb_grid_set_stream(jfftb_grid* g, void* stream);
 int jfftb_grid_synchronize(jfftb_grid* g);
 
+/* ---- input generators (microstructures.py:73-115) ------
+ * Scalar (pixel) fields of the grid, in place; `where` as above.  Host
+ * arrays are copied to the device, processed and copied back. */
+/* `passes` periodic passes of the separable binomial filter, one [1 2 1]/4
+ * sweep per axis (axis 0 first): gaussian_filter, microstructures.py:73-82,
+ * bit-identical to its NumPy rounding order (d-generic) */
+int jfftb_binomial_filter(jfftb_grid* g, double* field, int passes, int where);
+/* minimum and maximum of a field -> minmax2[0..1] (host) */
+int jfftb_field_minmax(jfftb_grid* g, const double* field, double* minmax2, int where);
+/* affine map onto [1/chi, 1], chi = inf -> [0, 1] (rescale_contrast,
+ * microstructures.py:104-115; same operation order); EINVAL for chi < 1 or a
+ * constant field */
+int jfftb_rescale_contrast(jfftb_grid* g, double* field, double chi, int where);
+/* 1 where v >= 0.5, else 1/chi (threshold, microstructures.py:94-101) */
+int jfftb_threshold(jfftb_grid* g, double* field, double chi, int where);
+/* BASELINE config-5 projection: v <- tanh(beta (v - 1/2)), min-max to
+ * [0, 1], E = emin + v^3 */
+int jfftb_simp_projection(jfftb_grid* g, double* field, double beta, double emin, int where);
+
 /* ---- FFT contract (grid.py:200-215 fft_forward / fft_inverse) ---------- */
 int jfftb_fft_forward(jfftb_grid* g, const double* u, double* spec, int where);
 int jfftb_fft_inverse(jfftb_grid* g, const double* spec, double* u, int where);

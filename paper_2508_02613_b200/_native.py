@@ -70,6 +70,11 @@ _SIGS = {
     "jfftb_profile_start": (C.c_int, [_P]),
     "jfftb_profile_read": (C.c_int, [_P, _D, _I64, C.c_int]),
     "jfftb_debug_fused_apply": (C.c_int, [_P, _P, C.c_int, _P, _P]),
+    "jfftb_binomial_filter": (C.c_int, [_P, _P, C.c_int, C.c_int]),
+    "jfftb_field_minmax": (C.c_int, [_P, _P, _D, C.c_int]),
+    "jfftb_rescale_contrast": (C.c_int, [_P, _P, C.c_double, C.c_int]),
+    "jfftb_threshold": (C.c_int, [_P, _P, C.c_double, C.c_int]),
+    "jfftb_simp_projection": (C.c_int, [_P, _P, C.c_double, C.c_double, C.c_int]),
 }
 EXPORTED = tuple(_SIGS)
 

@@ -1001,4 +1001,99 @@ int jfftb_profile_read(jfftb_grid* g, double* stage_ms, int64_t* iterations, int
   });
 }
 
+/* ---- input generators (generators.cu; microstructures.py:73-115) ------ */
+}  // extern "C"
+namespace {
+// run `body` on a device copy of a host scalar field (or in place on a
+// device field) and copy the result back
+template <class F>
+void scalar_inout(jfftb_grid* g, double* field, int where, F&& body) {
+  require(field != nullptr, "null field");
+  const int64_t n = g->geo.N;
+  if (where == JFFTB_DEVICE) {
+    body(field);
+    return;
+  }
+  require(where == JFFTB_HOST, "where must be JFFTB_HOST or JFFTB_DEVICE");
+  DevBuf tmp(sizeof(double) * n);
+  copy_h2d(g, tmp.ptr, field, sizeof(double) * n, g->stream);
+  body(tmp.as<double>());
+  copy_d2h(g, field, tmp.ptr, sizeof(double) * n, g->stream);
+}
+double* minmax_of(jfftb_grid* g, const double* field) {
+  double* part = ensure_partials(g, gen_partials(g->geo) + 2);
+  double* mm = part + gen_partials(g->geo);
+  launch_minmax(g->geo, g->stream, field, part, mm);
+  return mm;
+}
+}  // namespace
+extern "C" {
+
+int jfftb_binomial_filter(jfftb_grid* g, double* field, int passes, int where) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    require(passes >= 0, "filter passes must be >= 0");
+    DeviceGuard dg(g->device);
+    scalar_inout(g, field, where, [&](double* f) {
+      if (passes == 0) return;
+      DevBuf scratch(sizeof(double) * g->geo.N);
+      launch_binomial_filter(g->geo, g->stream, f, scratch.as<double>(), passes);
+      JF_CUDA(cudaStreamSynchronize(g->stream));
+    });
+  });
+}
+
+int jfftb_field_minmax(jfftb_grid* g, const double* field, double* minmax2, int where) {
+  return guarded([&] {
+    require(g != nullptr && minmax2 != nullptr, "null argument");
+    DeviceGuard dg(g->device);
+    DevBuf tin;
+    const double* f = stage_in(g, field, g->geo.N, where, tin);
+    double* mm = minmax_of(g, f);
+    JF_CUDA(cudaMemcpyAsync(minmax2, mm, 2 * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+int jfftb_rescale_contrast(jfftb_grid* g, double* field, double chi, int where) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    require(chi >= 1.0, "total phase contrast must be >= 1");
+    DeviceGuard dg(g->device);
+    const double soft = std::isinf(chi) ? 0.0 : 1.0 / chi;
+    scalar_inout(g, field, where, [&](double* f) {
+      double* mm = minmax_of(g, f);
+      double h[2];
+      JF_CUDA(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
+      JF_CUDA(cudaStreamSynchronize(g->stream));
+      require(h[1] > h[0], "cannot rescale a constant field to a target contrast");
+      launch_rescale(g->geo, g->stream, f, mm, soft);
+    });
+  });
+}
+
+int jfftb_threshold(jfftb_grid* g, double* field, double chi, int where) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    require(chi >= 1.0, "total phase contrast must be >= 1");
+    DeviceGuard dg(g->device);
+    const double soft = std::isinf(chi) ? 0.0 : 1.0 / chi;
+    scalar_inout(g, field, where, [&](double* f) { launch_threshold(g->geo, g->stream, f, soft); });
+  });
+}
+
+int jfftb_simp_projection(jfftb_grid* g, double* field, double beta, double emin, int where) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    require(std::isfinite(beta) && beta > 0.0, "projection sharpness must be finite and > 0");
+    require(std::isfinite(emin) && emin >= 0.0, "void stiffness must be finite and >= 0");
+    DeviceGuard dg(g->device);
+    scalar_inout(g, field, where, [&](double* f) {
+      double* part = ensure_partials(g, gen_partials(g->geo) + 2);
+      launch_simp(g->geo, g->stream, f, part, part + gen_partials(g->geo), beta, emin);
+      JF_CUDA(cudaStreamSynchronize(g->stream));
+    });
+  });
+}
+
 }  // extern "C"

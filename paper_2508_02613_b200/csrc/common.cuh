@@ -300,6 +300,17 @@ void copy_h2d(jfftb_grid* g, void* dst, const void* src, size_t bytes, cudaStrea
 void copy_d2h(jfftb_grid* g, void* dst, const void* src, size_t bytes, cudaStream_t s);
 void free_host_staging(jfftb_grid* g);
 
+// input generators (generators.cu)
+void launch_binomial_filter(const Geom& g, cudaStream_t s, double* field, double* scratch,
+                            int passes);
+void launch_minmax(const Geom& g, cudaStream_t s, const double* field, double* partial,
+                   double* out2);
+void launch_rescale(const Geom& g, cudaStream_t s, double* field, const double* mm, double soft);
+void launch_threshold(const Geom& g, cudaStream_t s, double* field, double soft);
+void launch_simp(const Geom& g, cudaStream_t s, double* field, double* partial, double* mm,
+                 double beta, double emin);
+int gen_partials(const Geom& g);
+
 // vector algebra
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic
 constexpr int kRedThreads = 256;

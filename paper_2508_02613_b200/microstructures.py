@@ -157,6 +157,22 @@ def crack_discs_device(n=512, count: int = 64, ell: float = 4.0, emin: float = 1
     return out
 
 
+def simp_density(n: int = 1024, filters: int = 8, beta: float = 8.0, emin: float = 1e-6,
+                 seed: int = 0) -> np.ndarray:
+    """Config 5 (host recipe): seeded uniform noise -> ``filters`` 3-D
+    binomial passes -> tanh(beta (rho - 1/2)) -> min-max to [0, 1] ->
+    SIMP E = emin + rho^3 (contrast ~1e6).  ``generators.simp_density_device``
+    runs the same steps in device memory for the 1024^3 grid."""
+    rng = np.random.default_rng(seed)
+    v = rng.random((n,) * 3)
+    for _ in range(filters):
+        v = binomial_filter(v)
+    v = np.tanh(beta * (v - 0.5))
+    lo, hi = v.min(), v.max()
+    v = (v - lo) / (hi - lo)
+    return emin + v * v * v
+
+
 def mandel_shear(d: int, i: int, j: int, gamma: float = 0.5) -> np.ndarray:
     """Mandel vector of the symmetric strain with eps_ij = eps_ji = gamma."""
     from .grid import mandel_index

@@ -104,3 +104,15 @@ def test_plugin_rebinds_reference_binding_sites():
     finally:
         plugin.unplug(saved)
     assert jfft.solver.pcg is orig
+
+
+def test_simp_density_host_recipe():
+    """BASELINE config 5 host recipe: seeded, range [emin, 1 + emin], the
+    threshold projection drives most voxels towards the two phases."""
+    from paper_2508_02613_b200 import microstructures as ms
+    a = ms.simp_density(24, filters=8, beta=8.0, emin=1e-6, seed=1)
+    b = ms.simp_density(24, filters=8, beta=8.0, emin=1e-6, seed=1)
+    assert np.array_equal(a, b)
+    assert a.min() == pytest.approx(1e-6, abs=1e-15)
+    assert a.max() == pytest.approx(1.0 + 1e-6, rel=1e-15)
+    assert a.shape == (24, 24, 24)
