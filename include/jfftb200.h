@@ -95,6 +95,12 @@ int jfftb_threshold(jfftb_grid* g, double* field, double chi, int where);
 /* BASELINE config-5 projection: v <- tanh(beta (v - 1/2)), min-max to
  * [0, 1], E = emin + v^3 */
 int jfftb_simp_projection(jfftb_grid* g, double* field, double beta, double emin, int where);
+/* field file layout (grid.py:225-295 save_field / load_field): convert
+ * `planes` consecutive planes between the file's "x1-fastest" order (Fortran
+ * order of the n0 x ... x n_{d-1} array) and C order: to_c = 1 file -> C,
+ * 0 C -> file.  Not in place. */
+int jfftb_field_layout(jfftb_grid* g, const double* src, double* dst, int planes, int to_c,
+                       int where);
 
 /* ---- FFT contract (grid.py:200-215 fft_forward / fft_inverse) ---------- */
 int jfftb_fft_forward(jfftb_grid* g, const double* u, double* spec, int where);

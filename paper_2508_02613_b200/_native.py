@@ -75,6 +75,7 @@ _SIGS = {
     "jfftb_rescale_contrast": (C.c_int, [_P, _P, C.c_double, C.c_int]),
     "jfftb_threshold": (C.c_int, [_P, _P, C.c_double, C.c_int]),
     "jfftb_simp_projection": (C.c_int, [_P, _P, C.c_double, C.c_double, C.c_int]),
+    "jfftb_field_layout": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int]),
 }
 EXPORTED = tuple(_SIGS)
 

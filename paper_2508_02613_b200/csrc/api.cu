@@ -1096,4 +1096,21 @@ int jfftb_simp_projection(jfftb_grid* g, double* field, double beta, double emin
   });
 }
 
+int jfftb_field_layout(jfftb_grid* g, const double* src, double* dst, int planes, int to_c,
+                       int where) {
+  return guarded([&] {
+    require(g != nullptr, "null grid");
+    require(planes >= 1, "planes must be >= 1");
+    DeviceGuard dg(g->device);
+    const size_t n = (size_t)planes * g->geo.N;
+    DevBuf tin, tout;
+    const double* ds = stage_in(g, src, n, where, tin);
+    double* dd = stage_out(dst, n, where, tout);
+    require(ds != dd, "field layout conversion cannot run in place");
+    launch_fortran_to_c(g->geo, g->stream, ds, dd, planes, to_c != 0);
+    finish_out(g, dst, dd, n, where);
+    if (where == JFFTB_DEVICE) JF_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
 }  // extern "C"

@@ -310,6 +310,8 @@ void launch_threshold(const Geom& g, cudaStream_t s, double* field, double soft)
 void launch_simp(const Geom& g, cudaStream_t s, double* field, double* partial, double* mm,
                  double beta, double emin);
 int gen_partials(const Geom& g);
+void launch_fortran_to_c(const Geom& g, cudaStream_t s, const double* src, double* dst,
+                         int planes, bool to_c);
 
 // vector algebra
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic

@@ -184,4 +184,46 @@ void launch_simp(const Geom& g, cudaStream_t s, double* field, double* partial, 
 
 int gen_partials(const Geom& g) { return 2 * gen_blocks(g.N) + 2; }
 
+// ---------------------------------------------------------------------------
+// field file layout (grid.py:225-295): every plane of the raw payload is
+// "x1-fastest" (Fortran order of the n0 x ... x n_{d-1} array).  Converting
+// between that and the C order of device fields swaps axes 0 and d-1 (the
+// middle axis of a 3-D field keeps its stride): a 32 x 32 tiled transpose
+// per (plane, middle index), coalesced on both sides.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void swap_outer_axes_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                       int na, int nm, int nb) {
+  // src viewed as [q][b][m][a] (a fastest), dst as [q][a][m][b] (b fastest)
+  __shared__ double tile[32][33];
+  const int64_t q = blockIdx.z / nm;
+  const int m = blockIdx.z % nm;
+  const int64_t plane = (int64_t)na * nm * nb;
+  const int a0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  const double* s = src + q * plane;
+  double* o = dst + q * plane;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int a = a0 + threadIdx.x, b = b0 + j;
+    if (a < na && b < nb) tile[j][threadIdx.x] = s[((int64_t)b * nm + m) * na + a];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int b = b0 + threadIdx.x, a = a0 + j;
+    if (a < na && b < nb) o[((int64_t)a * nm + m) * nb + b] = tile[threadIdx.x][j];
+  }
+}
+}  // namespace
+
+// planes of x1-fastest (Fortran) order <-> C order; to_c selects the direction
+void launch_fortran_to_c(const Geom& g, cudaStream_t s, const double* src, double* dst,
+                         int planes, bool to_c) {
+  const int n0 = g.n[0], nl = g.n[g.d - 1];
+  const int nm = g.d == 3 ? g.n[1] : 1;
+  // Fortran: axis 0 fastest -> viewed as [b = axis d-1][m][a = axis 0]
+  const int na = to_c ? n0 : nl, nb = to_c ? nl : n0;
+  dim3 grid((na + 31) / 32, (nb + 31) / 32, (unsigned)(planes * nm));
+  swap_outer_axes_kernel<<<grid, dim3(32, 8), 0, s>>>(src, dst, na, nm, nb);
+  JF_LAUNCHED();
+}
+
 }  // namespace jfftb
