@@ -77,6 +77,18 @@ int jfftb_grid_destroy(jfftb_grid* g);
 int jfftb_grid_set_stream(jfftb_grid* g, void* stream);
 int jfftb_grid_synchronize(jfftb_grid* g);
 
+/* ---- load cases (topopt.py:98-196 consumers of pcg) -----
+ * `nload` (1..6) solutions u (nload vector fields back to back, `where`)
+ * with macroscopic strains ebar (nload Mandel vectors, host).  Total strains
+ * eps_g = ebar_g + B u_g are paired per voxel,
+ *   P_gc(x) = sum_t eps_c^T C0 eps_g                (_strain_pairings)
+ * and sigma_out (nload x nload, host) = (w/|Y|) sum_x rho P_gc  (_stress_matrix).
+ * If field_out (N, `where`) is given, it receives sum_gc weights_gc P_gc(x)
+ * (weights: nload x nload host; _stress_gradient before its scale). */
+int jfftb_load_pairings(jfftb_op* op, int nload, const double* u, const double* ebar,
+                        const double* weights, double* sigma_out, double* field_out,
+                        int where);
+
 /* ---- input generators (microstructures.py:73-115) ------
  * Scalar (pixel) fields of the grid, in place; `where` as above.  Host
  * arrays are copied to the device, processed and copied back. */

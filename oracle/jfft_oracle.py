@@ -241,6 +241,22 @@ def homogenized_stress(rho, c, h, u, eps_bar, lengths):
     return scale * sig.sum(axis=tuple(range(1, d + 2)))
 
 
+def strain_pairings(c, h, us, loads):
+    """topopt.py:130-133 (_strain_pairings), d-generic: for solutions
+    ``us[g]`` of loads ``loads[g]``, P[g, c] = sum_t eps_c^T C0 eps_g per pixel."""
+    strains = np.stack([total_strain(h, u, e) for u, e in zip(us, loads)])
+    c_eps = np.einsum("mk,gkt...->gmt...", c, strains)
+    return np.einsum("cmt...,gmt...->gc...", strains, c_eps)
+
+
+def stress_matrix(rho, c, h, us, loads, lengths):
+    """topopt.py:136-141 (_stress_matrix): (w/|Y|) sum_x rho P[g, c]."""
+    d = rho.ndim
+    P = strain_pairings(c, h, us, loads)
+    return quad_weight(h) / float(np.prod(lengths)) * np.einsum(
+        "gc" + "xyz"[:d] + "," + "xyz"[:d] + "->gc", P, rho)
+
+
 # ---------------------------------------------------------------------------
 # preconditioners (preconditioners.py:50-136)
 # ---------------------------------------------------------------------------

@@ -76,6 +76,7 @@ _SIGS = {
     "jfftb_threshold": (C.c_int, [_P, _P, C.c_double, C.c_int]),
     "jfftb_simp_projection": (C.c_int, [_P, _P, C.c_double, C.c_double, C.c_int]),
     "jfftb_field_layout": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int]),
+    "jfftb_load_pairings": (C.c_int, [_P, C.c_int, _P, _D, _D, _D, _P, C.c_int]),
 }
 EXPORTED = tuple(_SIGS)
 

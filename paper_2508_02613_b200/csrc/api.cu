@@ -1113,4 +1113,43 @@ int jfftb_field_layout(jfftb_grid* g, const double* src, double* dst, int planes
   });
 }
 
+int jfftb_load_pairings(jfftb_op* op, int nload, const double* u, const double* ebar,
+                        const double* weights, double* sigma_out, double* field_out,
+                        int where) {
+  return guarded([&] {
+    require(op != nullptr && ebar != nullptr && sigma_out != nullptr, "null argument");
+    require(nload >= 1 && nload <= 6, "1 to 6 load cases");
+    jfftb_grid* g = op->grid;
+    const Geom& geo = g->geo;
+    const int M = geo.d == 2 ? 3 : 6;
+    for (int l = 0; l < nload; ++l) check_ebar(geo.d, ebar + l * M);
+    DeviceGuard dg(g->device);
+    DevBuf tin, tout, dw;
+    const double* du = stage_in(g, u, (size_t)nload * geo.d * geo.N, where, tin);
+    double* dfield = field_out ? stage_out(field_out, geo.N, where, tout) : nullptr;
+    if (field_out) {
+      require(weights != nullptr, "the pairing field needs load-pair weights");
+      dw.reset(sizeof(double) * nload * nload);
+      JF_CUDA(cudaMemcpyAsync(dw.ptr, weights, sizeof(double) * nload * nload,
+                              cudaMemcpyHostToDevice, g->stream));
+    }
+    const int K = nload * (nload + 1) / 2;
+    double* part = ensure_partials(g, kRedBlocks * K + K);
+    launch_load_pairings(geo, g->stream, nload, du, op->rho, op->lambda0, op->mu0, ebar,
+                         dw.as<double>(), dfield, part);
+    launch_sum_partials(g->stream, part, kRedBlocks, K, part + kRedBlocks * K);
+    std::vector<double> sums(K);
+    JF_CUDA(cudaMemcpyAsync(sums.data(), part + kRedBlocks * K, sizeof(double) * K,
+                            cudaMemcpyDeviceToHost, g->stream));
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+    double vol = 1.0;
+    for (int a = 0; a < geo.d; ++a) vol *= geo.h[a] * geo.n[a];
+    const double scale = geo.w / vol;
+    for (int a = 0, k = 0; a < nload; ++a)
+      for (int b = a; b < nload; ++b, ++k)
+        sigma_out[a * nload + b] = sigma_out[b * nload + a] = scale * sums[k];
+    if (field_out) finish_out(g, field_out, dfield, geo.N, where);
+  });
+}
+
 }  // extern "C"

@@ -313,6 +313,11 @@ int gen_partials(const Geom& g);
 void launch_fortran_to_c(const Geom& g, cudaStream_t s, const double* src, double* dst,
                          int planes, bool to_c);
 
+// energy pairings of load-case solutions (loadcases.cu); returns K
+int launch_load_pairings(const Geom& g, cudaStream_t s, int L, const double* u,
+                         const double* rho, double lam, double mu, const double* ebar,
+                         const double* wgt, double* field, double* partials);
+
 // vector algebra
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic
 constexpr int kRedThreads = 256;

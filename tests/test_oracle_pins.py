@@ -213,3 +213,32 @@ def test_generator_matches_reference_recipe():
         f = RM.gaussian_filter(f)
     f = RM.rescale_contrast(f, 1e4)
     assert np.array_equal(ms.bernoulli_smoothed(32, 4, 1e4, 3), f.values)
+
+
+def test_load_case_pairings_match_reference():
+    """oracle.strain_pairings / stress_matrix restate topopt.py:130-141; pinned
+    against the reference's own functions on random 2-D load solutions."""
+    ref = os.path.join("/root/reference", "pkg", "src")
+    if not os.path.isdir(ref):
+        pytest.skip("reference not mounted (GPU box)")
+    import sys
+    import types
+    sys.path.insert(0, ref)
+    from jfft import grid as RG, material as RMat, operators as RO, topopt as RT
+    rng = np.random.default_rng(4)
+    n, lengths = 12, (1.0, 1.5)
+    grid = RG.make_grid(n, lengths)
+    mat = RMat.isotropic_material(0.6, 0.35)
+    rho = rng.uniform(0.1, 1.0, (n, n))
+    us = rng.normal(size=(3, 2, n, n))
+    loads = np.eye(3)
+    op = RO.make_operator(RG.ScalarField(grid, rho), mat)
+    strains = np.stack([RO.total_strain(op, RG.VectorField(grid, us[g]), loads[g]).values
+                        for g in range(3)])
+    problem = types.SimpleNamespace(grid=grid, material=mat)
+    c = X.isotropic_stiffness(2, 0.6, 0.35)
+    h = X.pixel_size((n, n), lengths)
+    assert np.allclose(X.strain_pairings(c, h, us, loads), RT._strain_pairings(problem, strains),
+                       rtol=1e-13, atol=1e-13)
+    assert np.allclose(X.stress_matrix(rho, c, h, us, loads, lengths),
+                       RT._stress_matrix(problem, strains, rho), rtol=1e-13, atol=1e-15)
