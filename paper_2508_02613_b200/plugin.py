@@ -16,6 +16,9 @@ optimisation, CLI and Newton driver run on libjfftb200:
   experiments.{assemble_rhs, homogenized_stress, assemble_green,
                 build_preconditioner, pcg}
   topopt.{assemble_rhs, total_strain, assemble_green, build_preconditioner, pcg}
+  microstructures.{gaussian_filter, threshold, rescale_contrast, total_contrast}
+      (experiments.py:18 reaches them through the module object)
+  grid.{save_field, load_field}, experiments.{save_field, load_field}
   jfft.{...the same names}
 
 ``SystemOperator`` objects stay the reference's own (they are plain data);
@@ -27,6 +30,8 @@ from __future__ import annotations
 
 import importlib
 
+from . import fieldio as _fieldio
+from . import generators as _gen
 from . import operators as _ops
 from . import preconditioners as _pc
 from . import solver as _solver
@@ -40,8 +45,10 @@ _TARGETS = {
     "solver": ["apply_system", "residual_force", "apply_green", "assemble_green",
                "build_preconditioner", "pcg"],
     "experiments": ["assemble_rhs", "homogenized_stress", "assemble_green",
-                    "build_preconditioner", "pcg"],
+                    "build_preconditioner", "pcg", "save_field", "load_field"],
     "topopt": ["assemble_rhs", "total_strain", "assemble_green", "build_preconditioner", "pcg"],
+    "microstructures": ["gaussian_filter", "threshold", "rescale_contrast", "total_contrast"],
+    "grid": ["save_field", "load_field"],
     "": ["apply_system", "assemble_rhs", "total_strain", "residual_force", "homogenized_stress",
          "apply_green", "apply_jacobi", "apply_jacobi_half", "apply_green_jacobi",
          "assemble_green", "assemble_jacobi", "build_preconditioner", "Preconditioner", "pcg"],
@@ -56,7 +63,14 @@ def _replacement(name: str, ref_solver):
                                abort_error=ref_solver.SolverAbortError)
         pcg.__doc__ = _solver.pcg.__doc__
         return pcg
-    for mod in (_ops, _pc, _solver):
+    if name == "load_field":
+        ref_grid = importlib.import_module(ref_solver.__name__.rsplit(".", 1)[0] + ".grid")
+
+        def load_field(basepath):
+            return _fieldio.load_field(basepath, module=ref_grid)
+        load_field.__doc__ = _fieldio.load_field.__doc__
+        return load_field
+    for mod in (_ops, _pc, _solver, _gen, _fieldio):
         if hasattr(mod, name):
             return getattr(mod, name)
     raise AttributeError(name)

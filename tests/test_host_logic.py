@@ -101,6 +101,14 @@ def test_plugin_rebinds_reference_binding_sites():
         assert jfft.experiments.assemble_green is plugin._replacement("assemble_green", jfft.solver)
         assert jfft.preconditioners.apply_system is plugin._replacement("apply_system", jfft.solver)
         assert len(saved) >= 30
+        import jfft.microstructures
+        from paper_2508_02613_b200 import generators
+        assert jfft.microstructures.gaussian_filter is generators.gaussian_filter
+        # the field-file loader returns the reference's own containers
+        fix = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fields", "vector")
+        f = jfft.experiments.load_field(fix)
+        assert type(f) is jfft.grid.VectorField
+        assert np.array_equal(f.values, np.load(fix[:-6] + "values.npz")["vector"])
     finally:
         plugin.unplug(saved)
     assert jfft.solver.pcg is orig
