@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fft.cuh"
 
 namespace jfftb {
 
@@ -690,7 +691,7 @@ int jfftb_green_create_slab(jfftb_grid* g, double lambda_ref, double mu_ref, int
     }
     const int layout = slab ? 2 + (k1_lo | (k1_count << 20)) : (g->fused ? 1 : 0);
     launch_green_setup(geo, g->stream, resp.as<double>(), m[0] | (m[1] << 8) | (m[2] << 16),
-                       gr->blocks, layout, nfreq);
+                       gr->blocks, layout, nfreq, layout == 1 && fused_dif());
     JF_CUDA(cudaStreamSynchronize(g->stream));
     g->refs.fetch_add(1);
     *out = gr;
@@ -762,6 +763,7 @@ int jfftb_green_export_blocks(jfftb_green* green, double* out) {
           for (int a = 0; a < d; ++a) q[a] = (geo.n[a] - q[a]) % geo.n[a];
           conj = -1.0;
         }
+        if (fused_dif()) q[d - 1] = dif_pos(geo.n[d - 1], q[d - 1]);  // in-place pass C slots
         src = q[0];
         for (int a = 1; a < d; ++a) src = src * geo.n[a] + q[a];
       }

@@ -294,6 +294,12 @@ void launch_total_strain(const Geom& g, cudaStream_t s, const double* u,
 int launch_stress_sum(const Geom& g, cudaStream_t s, const double* u, const double* rho,
                       double lam, double mu, const double* ebar, double* partials);
 
+// pass C transforms the last axis in place (DIF forward / DIT inverse), so
+// the fused-layout Green planes are stored with the last axis in the
+// transform's digit-reversed slot order (fft.cuh dif_pos); JFFTB_PASSC_DIF=0
+// selects the Stockham pass C and natural order (read once per process)
+bool fused_dif();
+
 // host <-> device field copies (hostio.cu): pageable host memory is staged
 // through a pinned ring by a team of host threads; d2h returns synchronised
 void copy_h2d(jfftb_grid* g, void* dst, const void* src, size_t bytes, cudaStream_t s);
@@ -340,7 +346,7 @@ void launch_green_apply(const Geom& g, cudaStream_t s, const double* blocks,
 // layout 0: numpy rfftn order (last axis halved), nfreq = Nh; layout 1:
 // fused.cu order (axis 0 halved), nfreq = fused_spec_elems
 void launch_green_setup(const Geom& g, cudaStream_t s, const double* resp, int m,
-                        double* blocks, int layout, int64_t nfreq);
+                        double* blocks, int layout, int64_t nfreq, bool dif_last = false);
 
 // PCG (pcg.cu)
 struct PcgBuffers {

@@ -280,6 +280,120 @@ __device__ __forceinline__ void cta_fft_io(double2* buf, int ks, int qs,
                                                                       gqs, gks);
 }
 
+// ---------------------------------------------------------------------------
+// In-place mixed-radix transforms (radix-8 stages, one trailing 2 or 4):
+// forward decimation in frequency (natural order in, digit-reversed out),
+// inverse decimation in time (digit-reversed in, natural out).  Every thread
+// reads and writes the same R elements of a stage, so a stage needs one
+// barrier (after its writes) instead of the Stockham schedule's two.  Stage s
+// of length-L sequences works on blocks of P_s = L / (R_0 ... R_{s-1})
+// elements; butterfly (block, j < Q = P_s / R_s) takes elements
+// block P_s + j + Q t.  Forward: DFT_R, then output t times w_P^(j t);
+// inverse: input t times conj(w_P^(j t)), then the inverse DFT_R (no 1/L).
+// Frequency k of the forward transform sits at slot dif_pos(L, k).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int fft_span(int L, int s) {
+  int p = L;
+  for (int i = 0; i < s; ++i) p /= fft_radix(L, i);
+  return p;
+}
+__host__ __device__ constexpr int dif_pos(int L, int k) {
+  int pos = 0, block = L;
+  for (int s = 0; s < fft_nstages(L); ++s) {
+    const int R = fft_radix(L, s);
+    block /= R;
+    pos += (k % R) * block;
+    k /= R;
+  }
+  return pos;
+}
+__host__ __device__ constexpr int dif_freq(int L, int p) {
+  int k = 0, mult = 1, block = L;
+  for (int s = 0; s < fft_nstages(L); ++s) {
+    const int R = fft_radix(L, s);
+    block /= R;
+    k += (p / block) * mult;
+    p %= block;
+    mult *= R;
+  }
+  return k;
+}
+
+// one in-place stage; sequences are contiguous rows at buf + q * qs (element
+// e at pidx<PAD>(e)); GIN: forward stage 0 reads gin + q * gqs + e; GOUT:
+// inverse stage 0 writes gout + q * gqs + e instead of buf
+template <int L, int NSEQ, int NT, bool INV, int PAD, int S, bool GIN, bool GOUT>
+__device__ __forceinline__ void cta_fft_ip_stage(double2* buf, int qs,
+                                                 const double2* __restrict__ tw,
+                                                 const double2* gin, double2* gout,
+                                                 int64_t gqs) {
+  constexpr int R = fft_radix(L, S);
+  constexpr int P = fft_span(L, S);
+  constexpr int Q = P / R;
+  constexpr int NB = L / R;          // butterflies per sequence
+  constexpr int B = NSEQ * NB;
+  constexpr int PER = (B + NT - 1) / NT;
+  constexpr bool FROM_G = GIN && !INV && S == 0;
+  constexpr bool TO_G = GOUT && INV && S == 0;
+  const double2* __restrict__ tws = tw + tw_stage_off(P, R);
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    const int b = threadIdx.x + m * NT;
+    if (B % NT == 0 || b < B) {
+      const int q = b / NB, bb = b % NB;
+      const int j = bb % Q;
+      const int base = (bb / Q) * P + j;
+      double2 v[8];
+      if constexpr (FROM_G) {
+        const double2* src = gin + q * gqs;
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = src[base + Q * t];
+      } else {
+        const double2* src = buf + q * qs;
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = src[pidx<PAD>(base + Q * t)];
+      }
+      if (INV && Q > 1) {
+#pragma unroll
+        for (int t = 1; t < R; ++t) v[t] = cmulc(v[t], __ldg(tws + (t - 1) * Q + j));
+      }
+      dftR<R, INV>(v);
+      if (!INV && Q > 1) {
+#pragma unroll
+        for (int t = 1; t < R; ++t) v[t] = cmul(v[t], __ldg(tws + (t - 1) * Q + j));
+      }
+      if constexpr (TO_G) {
+        double2* dst = gout + q * gqs;
+#pragma unroll
+        for (int t = 0; t < R; ++t) dst[base + Q * t] = v[t];
+      } else {
+        double2* dst = buf + q * qs;
+#pragma unroll
+        for (int t = 0; t < R; ++t) dst[pidx<PAD>(base + Q * t)] = v[t];
+      }
+    }
+  }
+  if constexpr (!TO_G) __syncthreads();
+}
+
+template <int L, int NSEQ, int NT, int PAD, bool GIN, int S = 0>
+__device__ __forceinline__ void cta_fft_dif(double2* buf, int qs, const double2* __restrict__ tw,
+                                            const double2* gin, int64_t gqs) {
+  if constexpr (S < fft_nstages(L)) {
+    cta_fft_ip_stage<L, NSEQ, NT, false, PAD, S, GIN, false>(buf, qs, tw, gin, nullptr, gqs);
+    cta_fft_dif<L, NSEQ, NT, PAD, GIN, S + 1>(buf, qs, tw, gin, gqs);
+  }
+}
+template <int L, int NSEQ, int NT, int PAD, bool GOUT, int S = fft_nstages(L) - 1>
+__device__ __forceinline__ void cta_fft_dit_inv(double2* buf, int qs,
+                                                const double2* __restrict__ tw, double2* gout,
+                                                int64_t gqs) {
+  if constexpr (S >= 0) {
+    cta_fft_ip_stage<L, NSEQ, NT, true, PAD, S, false, GOUT>(buf, qs, tw, nullptr, gout, gqs);
+    cta_fft_dit_inv<L, NSEQ, NT, PAD, GOUT, S - 1>(buf, qs, tw, gout, gqs);
+  }
+}
+
 // exp(-2 pi i j / 4096), j < 4096
 void launch_twiddles(cudaStream_t s, double2* tw);
 

@@ -261,7 +261,7 @@ constexpr int passC_minb(int D, int L, int F, bool GS = true) {
                                                    : (passC_bufd(D, L, F, GS) * 8 <= 110 * 1024 ? 2 : 1);
 }
 
-template <int D, int L, int F, int MODE, bool GS>
+template <int D, int L, int F, int MODE, bool GS, bool IP>
 __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     passC(FGeom g, const PcgState* __restrict__ st, const double* __restrict__ gpc,
           const double* __restrict__ gterm, double2* __restrict__ spec,
@@ -306,8 +306,11 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     const double w = (k0 == 0 || 2 * k0 == g.n0) ? 1.0 : 2.0;
     // forward: global rows -> (stage 1) -> shared; barrier-separated from the
     // previous row-set's last shared-memory reads by the loop-end barrier
-    cta_fft_io<L, NQ, NT, false, false, CPAD, true, false>(sbuf, 1, RL, tw, spec + rbase, nullptr,
-                                                           g.CS, 1);
+    if constexpr (IP)
+      cta_fft_dif<L, NQ, NT, CPAD, true>(sbuf, RL, tw, spec + rbase, g.CS);
+    else
+      cta_fft_io<L, NQ, NT, false, false, CPAD, true, false>(sbuf, 1, RL, tw, spec + rbase,
+                                                             nullptr, g.CS, 1);
     if (GS) mbar_wait(&gbar, gphase);  // this row-set's Green planes
     gphase ^= 1;
     __syncthreads();
@@ -357,9 +360,14 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     }
     __syncthreads();  // block solve done: Green planes and r^ rows are free
     if (row + gridDim.x < rows) prefetch_green(row + gridDim.x);
-    if (MODE != FM_QUAD)
-      cta_fft_io<L, D, NT, true, false, CPAD, false, true>(sbuf + ZQ * RL, 1, RL, tw, nullptr,
-                                                           spec + ZQ * g.CS + rbase, g.CS, 1);
+    if (MODE != FM_QUAD) {
+      if constexpr (IP)
+        cta_fft_dit_inv<L, D, NT, CPAD, true>(sbuf + ZQ * RL, RL, tw, spec + ZQ * g.CS + rbase,
+                                              g.CS);
+      else
+        cta_fft_io<L, D, NT, true, false, CPAD, false, true>(sbuf + ZQ * RL, 1, RL, tw, nullptr,
+                                                             spec + ZQ * g.CS + rbase, g.CS, 1);
+    }
     __syncthreads();
   }
   if (MODE != FM_APPLY) {
@@ -526,7 +534,7 @@ int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* 
   constexpr int NT = passC_nt(D, L, F);
   constexpr int BUFD = passC_bufd(D, L, F, kGStage);
   const size_t smem = sizeof(double) * BUFD;
-  auto k = passC<D, L, F, MODE, kGStage>;
+  auto k = fused_dif() ? passC<D, L, F, MODE, kGStage, true> : passC<D, L, F, MODE, kGStage, false>;
   static int per_sm = -1;  // per instantiation
   if (per_sm < 0) {
     set_smem(k, smem);
@@ -619,6 +627,14 @@ void launch_twiddles(cudaStream_t s, double2* tw) {
   JF_LAUNCHED();
   twiddle_stage_kernel<<<dim3(kTwN / 256, 13, 3), 256, 0, s>>>(tw);
   JF_LAUNCHED();
+}
+
+bool fused_dif() {
+  static const bool v = [] {
+    const char* e = std::getenv("JFFTB_PASSC_DIF");
+    return !(e && e[0] == '0');
+  }();
+  return v;
 }
 
 bool fused_supported(const Geom& g) {
