@@ -322,11 +322,14 @@ __host__ __device__ constexpr int dif_freq(int L, int p) {
 // one in-place stage; sequences are contiguous rows at buf + q * qs (element
 // e at pidx<PAD>(e)); GIN: forward stage 0 reads gin + q * gqs + e; GOUT:
 // inverse stage 0 writes gout + q * gqs + e instead of buf
-template <int L, int NSEQ, int NT, bool INV, int PAD, int S, bool GIN, bool GOUT>
+// QF: interleaved sequences (element e of sequence q at buf[e * ks + q],
+// consecutive threads take consecutive sequences); otherwise rows at
+// buf + q * qs with consecutive threads on consecutive butterflies
+template <int L, int NSEQ, int NT, bool INV, int PAD, int S, bool GIN, bool GOUT, bool QF = false>
 __device__ __forceinline__ void cta_fft_ip_stage(double2* buf, int qs,
                                                  const double2* __restrict__ tw,
                                                  const double2* gin, double2* gout,
-                                                 int64_t gqs) {
+                                                 int64_t gqs, int ks = 1) {
   constexpr int R = fft_radix(L, S);
   constexpr int P = fft_span(L, S);
   constexpr int Q = P / R;
@@ -340,7 +343,7 @@ __device__ __forceinline__ void cta_fft_ip_stage(double2* buf, int qs,
   for (int m = 0; m < PER; ++m) {
     const int b = threadIdx.x + m * NT;
     if (B % NT == 0 || b < B) {
-      const int q = b / NB, bb = b % NB;
+      const int q = QF ? b % NSEQ : b / NB, bb = QF ? b / NSEQ : b % NB;
       const int j = bb % Q;
       const int base = (bb / Q) * P + j;
       double2 v[8];
@@ -348,6 +351,9 @@ __device__ __forceinline__ void cta_fft_ip_stage(double2* buf, int qs,
         const double2* src = gin + q * gqs;
 #pragma unroll
         for (int t = 0; t < R; ++t) v[t] = src[base + Q * t];
+      } else if constexpr (QF) {
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = buf[(base + Q * t) * ks + q];
       } else {
         const double2* src = buf + q * qs;
 #pragma unroll
@@ -366,6 +372,9 @@ __device__ __forceinline__ void cta_fft_ip_stage(double2* buf, int qs,
         double2* dst = gout + q * gqs;
 #pragma unroll
         for (int t = 0; t < R; ++t) dst[base + Q * t] = v[t];
+      } else if constexpr (QF) {
+#pragma unroll
+        for (int t = 0; t < R; ++t) buf[(base + Q * t) * ks + q] = v[t];
       } else {
         double2* dst = buf + q * qs;
 #pragma unroll
@@ -384,6 +393,17 @@ __device__ __forceinline__ void cta_fft_dif(double2* buf, int qs, const double2*
     cta_fft_dif<L, NSEQ, NT, PAD, GIN, S + 1>(buf, qs, tw, gin, gqs);
   }
 }
+// forward in-place DIF of interleaved sequences, stages S.. (S0 = 1 when the
+// caller did stage 0 in registers)
+template <int L, int NSEQ, int NT, int S>
+__device__ __forceinline__ void cta_fft_dif_qf(double2* buf, int ks, const double2* __restrict__ tw) {
+  if constexpr (S < fft_nstages(L)) {
+    cta_fft_ip_stage<L, NSEQ, NT, false, 0, S, false, false, true>(buf, 0, tw, nullptr, nullptr, 0,
+                                                                   ks);
+    cta_fft_dif_qf<L, NSEQ, NT, S + 1>(buf, ks, tw);
+  }
+}
+
 template <int L, int NSEQ, int NT, int PAD, bool GOUT, int S = fft_nstages(L) - 1>
 __device__ __forceinline__ void cta_fft_dit_inv(double2* buf, int qs,
                                                 const double2* __restrict__ tw, double2* gout,

@@ -141,7 +141,9 @@ __global__ void __launch_bounds__(passA_nt(M, F, TW), passA_nt(M, F, TW) <= 512 
     }
   }
   __syncthreads();
+#ifndef JF_PASSA_NOFFT
   cta_fft<M, FTW, NT, false>(sbuf, FTW, 1, tw);
+#endif
   // unpack the packed half-length transforms into X[k], k = 0..M, pairwise:
   // X[k] and X[M-k] come from the same two entries z[k], z[M-k] (k = 0
   // pairs with the Nyquist row M), so each entry is read once
@@ -159,6 +161,102 @@ __global__ void __launch_bounds__(passA_nt(M, F, TW), passA_nt(M, F, TW) <= 512 
     const double2 za = sbuf[k * FTW + q];
     const double2 zb = sbuf[(kc % M) * FTW + q];
     double2* out = spec + (f * g.d + c) * g.CS + col0 + col;
+    out[(int64_t)k * g.PS] = unpack(za, cconj(zb), k);
+    if (kc != k) out[(int64_t)kc * g.PS] = unpack(zb, cconj(za), kc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pass A, green-jacobi (F = 2) INIT / ITER with the first transform stage in
+// registers: thread (col, j) loads exactly the 2 R0 real rows its stage-0
+// radix-R0 butterfly needs (packed entries j + Q0 t) for both fields, so the
+// tile is never staged through shared memory before the transform and the
+// remaining stages run in place (DIF, one barrier each).  The unpack reads
+// the digit-reversed slots (fft.cuh dif_pos).  Same tile, same traffic.
+// ---------------------------------------------------------------------------
+template <int M>
+constexpr int passA3_nt() { return tw_a(M) * (M / fft_radix(M, 0)); }
+template <int M>
+constexpr bool passA3_ok() { return passA3_nt<M>() >= 64 && passA3_nt<M>() <= 1024; }
+
+template <int M, int MODE>
+__global__ void __launch_bounds__(passA3_nt<M>(), 1)
+    passA3(FGeom g, const PcgState* __restrict__ st, double* __restrict__ r,
+           const double* __restrict__ kp, const double* __restrict__ dinv,
+           double2* __restrict__ spec, const double2* __restrict__ tw) {
+  constexpr int TW = tw_a(M);
+  constexpr int FTW = 2 * TW;         // sequences: [field][col]
+  constexpr int NT = passA3_nt<M>();
+  constexpr int R0 = fft_radix(M, 0);
+  constexpr int Q0 = M / R0;
+  static_assert(MODE == FM_ITER || MODE == FM_INIT, "pass A3 runs the PCG modes");
+  extern __shared__ double2 sbuf[];   // [m][field][col]
+  if (st->done) return;
+  const int c = blockIdx.y;
+  const int64_t col0 = (int64_t)blockIdx.x * TW;
+  const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
+  const int col = threadIdx.x % TW, j = threadIdx.x / TW;
+  double* rc = r + c * g.N + col0 + col;
+  const double* kc = kp + c * g.N + col0 + col;
+  const double* dc = dinv + c * g.N + col0 + col;
+  double a[R0][2], kv[R0][2], dv[R0][2];
+#pragma unroll
+  for (int t = 0; t < R0; ++t)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t gi = (int64_t)(2 * (j + Q0 * t) + h) * g.PS;
+      a[t][h] = rc[gi];
+      if (MODE == FM_ITER) kv[t][h] = kc[gi];
+      dv[t][h] = __ldg(dc + gi);
+    }
+  double2 v0[8], v1[8];
+#pragma unroll
+  for (int t = 0; t < R0; ++t) {
+    double x[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      x[h] = a[t][h];
+      if (MODE == FM_ITER) {
+        x[h] = x[h] - alpha * kv[t][h];
+        rc[(int64_t)(2 * (j + Q0 * t) + h) * g.PS] = x[h];
+      }
+    }
+    v0[t] = make_double2(x[0], x[1]);
+    v1[t] = make_double2(dv[t][0] * x[0], dv[t][1] * x[1]);  // s = D^-1/2 r'
+  }
+  dftR<R0, false>(v0);
+  dftR<R0, false>(v1);
+  if constexpr (Q0 > 1) {
+    const double2* __restrict__ tws = tw + tw_stage_off(M, R0);
+#pragma unroll
+    for (int t = 1; t < R0; ++t) {
+      const double2 w = __ldg(tws + (t - 1) * Q0 + j);
+      v0[t] = cmul(v0[t], w);
+      v1[t] = cmul(v1[t], w);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < R0; ++t) {
+    sbuf[(j + Q0 * t) * FTW + col] = v0[t];
+    sbuf[(j + Q0 * t) * FTW + TW + col] = v1[t];
+  }
+  __syncthreads();
+  cta_fft_dif_qf<M, FTW, NT, 1>(sbuf, FTW, tw);
+  // unpack X[k], k = 0..M, pairwise (k, M - k) from the digit-reversed slots
+  constexpr int TWS = kTwN / (2 * M);
+  auto unpack = [&](double2 zk, double2 zc, int k) {
+    const double2 fe = cscale(cadd(zk, zc), 0.5);
+    const double2 fo = cscale(csub(zk, zc), 0.5);                   // = i Fo
+    const double2 w = __ldg(tw + ((k * TWS) & (kTwN - 1)));         // e^{-2 pi i k / n0}
+    return cadd(fe, cmul(w, mul_mi<false>(fo)));                    // Fe + w Fo
+  };
+  for (int e = threadIdx.x; e < (M / 2 + 1) * FTW; e += NT) {
+    const int k = e / FTW, q = e % FTW;
+    const int f = q / TW, cl = q % TW;
+    const int kc = M - k;
+    const double2 za = sbuf[dif_pos(M, k) * FTW + q];
+    const double2 zb = sbuf[dif_pos(M, kc % M) * FTW + q];
+    double2* out = spec + (f * g.d + c) * g.CS + col0 + cl;
     out[(int64_t)k * g.PS] = unpack(za, cconj(zb), k);
     if (kc != k) out[(int64_t)kc * g.PS] = unpack(zb, cconj(za), kc);
   }
@@ -510,9 +608,31 @@ void launchA_MT(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, c
   k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
   JF_LAUNCHED();
 }
+// JFFTB_PASSA3=0 keeps the Stockham green-jacobi tile (A/B measurements)
+inline bool passA3_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("JFFTB_PASSA3");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 template <int M, int F, int MODE>
 void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, const double* kp,
                const double* dinv, double2* spec, const double2* tw) {
+  if constexpr (F == 2 && MODE != FM_APPLY && passA3_ok<M>()) {
+    if (passA3_enabled()) {
+      constexpr int TW = tw_a(M);
+      constexpr int NT = passA3_nt<M>();
+      const size_t smem = sizeof(double2) * 2 * TW * M;
+      auto k = passA3<M, MODE>;
+      static bool attr = false;
+      if (!attr) { set_smem(k, smem); attr = true; }
+      dim3 grid((unsigned)(g.PS / TW), g.d);
+      k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
+      JF_LAUNCHED();
+      return;
+    }
+  }
   launchA_MT<M, F, MODE, tw_a(M)>(g, s, st, r, kp, dinv, spec, tw);
 }
 template <int L, bool INV, bool PRED>
