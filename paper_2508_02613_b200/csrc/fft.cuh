@@ -385,12 +385,13 @@ __device__ __forceinline__ void cta_fft_ip_stage(double2* buf, int qs,
   if constexpr (!TO_G) __syncthreads();
 }
 
-template <int L, int NSEQ, int NT, int PAD, bool GIN, int S = 0>
+// stages S .. END-1 (END < nstages leaves the last stages to the caller)
+template <int L, int NSEQ, int NT, int PAD, bool GIN, int S = 0, int END = fft_nstages(L)>
 __device__ __forceinline__ void cta_fft_dif(double2* buf, int qs, const double2* __restrict__ tw,
                                             const double2* gin, int64_t gqs) {
-  if constexpr (S < fft_nstages(L)) {
+  if constexpr (S < END) {
     cta_fft_ip_stage<L, NSEQ, NT, false, PAD, S, GIN, false>(buf, qs, tw, gin, nullptr, gqs);
-    cta_fft_dif<L, NSEQ, NT, PAD, GIN, S + 1>(buf, qs, tw, gin, gqs);
+    cta_fft_dif<L, NSEQ, NT, PAD, GIN, S + 1, END>(buf, qs, tw, gin, gqs);
   }
 }
 // forward in-place DIF of interleaved sequences, stages S.. (S0 = 1 when the

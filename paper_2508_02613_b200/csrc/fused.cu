@@ -141,9 +141,7 @@ __global__ void __launch_bounds__(passA_nt(M, F, TW), passA_nt(M, F, TW) <= 512 
     }
   }
   __syncthreads();
-#ifndef JF_PASSA_NOFFT
   cta_fft<M, FTW, NT, false>(sbuf, FTW, 1, tw);
-#endif
   // unpack the packed half-length transforms into X[k], k = 0..M, pairwise:
   // X[k] and X[M-k] come from the same two entries z[k], z[M-k] (k = 0
   // pairs with the Nyquist row M), so each entry is read once
@@ -652,8 +650,7 @@ template <int D, int L, int F, int MODE>
 int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* gpc,
               const double* gterm, double2* spec, double* partials, const double2* tw) {
   constexpr int NT = passC_nt(D, L, F);
-  constexpr int BUFD = passC_bufd(D, L, F, kGStage);
-  const size_t smem = sizeof(double) * BUFD;
+  const size_t smem = sizeof(double) * passC_bufd(D, L, F, kGStage);
   auto k = fused_dif() ? passC<D, L, F, MODE, kGStage, true> : passC<D, L, F, MODE, kGStage, false>;
   static int per_sm = -1;  // per instantiation
   if (per_sm < 0) {

@@ -86,8 +86,14 @@ __host__ EbarT make_ebar(int d, const double* m) {
 // displacements are read from the ring, forces for the +x neighbour travel by
 // warp shuffle and the combined +y forces through a double-buffered smem row.
 // One __syncthreads per layer.
-constexpr int S3_U = 3 * 3 * (BY3 + 1) * (BX3 + 1);  // u ring: [slot][comp][y][x]
-constexpr int S3_R = 3 * BY3 * BX3;                  // rho ring: [slot][y][x]
+// ring depth: plane kk + RING - 1 is requested while layer kk is computed
+#ifndef JF_ST_RING
+#define JF_ST_RING 3
+#endif
+constexpr int RING = JF_ST_RING;
+static_assert(RING == 3 || RING == 4, "plane ring of 3 or 4 slots");
+constexpr int S3_U = RING * 3 * (BY3 + 1) * (BX3 + 1);  // u ring: [slot][comp][y][x]
+constexpr int S3_R = RING * BY3 * BX3;                  // rho ring: [slot][y][x]
 constexpr int S3_F = 2 * 2 * 3 * BY3 * BX3;          // +y hand-over: [buf][plane][comp][y][x]
 constexpr size_t S3_BYTES = sizeof(double) * (S3_U + S3_R + S3_F + 32);
 
@@ -158,7 +164,8 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   // async fetch of layer kk (unwrapped, -1 <= kk <= n0 + 2) into ring slot
   // (kk+3)%3; plane wrap by compare (no integer division in the march)
   auto plane_of = [&](int kk) { return kk < 0 ? kk + n0 : (kk >= n0 ? kk - n0 : kk); };
-  auto slot_of = [](int kk) { return (kk + 3) % 3; };
+  auto slot_of = [](int kk) { return (kk + RING) % RING; };
+  auto next_slot = [](int sl) { return sl == RING - 1 ? 0 : sl + 1; };
   auto fetch_u = [&](int kk, int s) {
     if (!HAS_U) return;
     const double* ub = u + (int64_t)plane_of(kk) * P;
@@ -184,17 +191,21 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int i = 0; i < 3; ++i) uk[q][i] = uk1[q][i] = 0.0;
-  // prologue: group A = planes k0-1, k0 and rho(k0-1); group B = plane k0+1, rho(k0)
+  // prologue: group A = planes k0-1, k0 and rho(k0-1); then one group per
+  // plane k0+i with rho(k0+i-1), i = 1 .. RING-2
   int s0 = slot_of(k0 - 1);                   // slot of layer kk (rotates by one)
-  int s1 = s0 == 2 ? 0 : s0 + 1, s2 = s1 == 2 ? 0 : s1 + 1;
+  int s1 = next_slot(s0);
   fetch_u(k0 - 1, s0);
   fetch_u(k0, s1);
   fetch_r(k0 - 1, s0);
   cp_async_commit();
-  fetch_u(k0 + 1, s2);
-  fetch_r(k0, s1);
-  cp_async_commit();
-  cp_async_wait<1>();
+#pragma unroll
+  for (int i = 1; i <= RING - 2; ++i) {
+    fetch_u(k0 + i, slot_of(k0 - 1 + i + 1));
+    fetch_r(k0 + i - 1, slot_of(k0 - 1 + i));
+    cp_async_commit();
+  }
+  cp_async_wait<RING - 2>();
   __syncthreads();
 
   double nxt[3] = {0.0, 0.0, 0.0};
@@ -202,7 +213,8 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   int64_t obase = (int64_t)plane_of(k0 - 1) * P + col;  // output index of layer kk
   for (int kk = k0 - 1, j = 0; kk < k1; ++kk, ++j) {
     const int b = j & 1;
-    // slots: s0 = layer kk (u plane kk, rho kk), s1 = kk + 1, s2 = kk + 2.
+    // slots: s0 = layer kk (u plane kk, rho kk), s1 = kk + 1; planes up to
+    // kk + RING - 1 are in flight
     // Both corner planes are read from the ring (no register hand-over
     // between layers); the slots are refilled after this layer's barrier.
     if (HAS_U) {
@@ -240,7 +252,7 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
       Fy[b][1][i][ty][tx] = f[3][i] + (tx >= 1 ? y1 : 0.0);
 #endif
     }
-    cp_async_wait<0>();  // plane kk+2 / rho(kk+1) landed (needed next layer)
+    cp_async_wait<RING - 3>();  // plane kk+2 / rho(kk+1) landed (needed next layer)
     __syncthreads();     // ... and every warp is done reading slot s0
     if (ty >= 1) {
 #pragma unroll
@@ -257,13 +269,13 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
     }
     obase += P;
     if (obase >= g.N) obase -= g.N;
-    // refill: plane kk+3 takes plane kk's slot, rho(kk+2) takes rho(kk-1)'s
-    if (kk + 3 <= k1) fetch_u(kk + 3, s0);
-    if (kk + 2 < k1) fetch_r(kk + 2, s2);
+    // refill: plane kk+RING takes plane kk's slot, rho(kk+RING-1) takes
+    // rho(kk-1)'s
+    if (kk + RING <= k1) fetch_u(kk + RING, s0);
+    if (kk + RING - 1 < k1) fetch_r(kk + RING - 1, slot_of(kk + RING - 1));
     cp_async_commit();
     s0 = s1;
-    s1 = s2;
-    s2 = s2 == 2 ? 0 : s2 + 1;
+    s1 = next_slot(s1);
   }
   cp_async_wait<0>();
   if (MODE == VOX_K && partials) {
