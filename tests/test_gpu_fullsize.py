@@ -1,0 +1,137 @@
+"""Size-independent properties at the bench size (BASELINE config 4: 512^3
+crack-disc damage field), where no CPU oracle fits (a NumPy restatement
+would need ~40 GB of quadrature fields).  Everything stays on the device;
+the checks use torch fp64 reductions as the independent arithmetic.
+
+* K is symmetric: <u, K v> = <K u, v>;
+* rigid translations are in its null space: K c = 0;
+* the Green operator inverts the reference operator on mean-free fields:
+  G K_ref u = u - mean(u) (preconditioners.py:50-80 contract);
+* the fused Green-Jacobi application equals its composition
+  D^-1/2 (G (D^-1/2 r)) (preconditioners.py:132-136);
+* the PCG recurrence agrees with the true residual: after a capped
+  Green-Jacobi solve, <r, G r> of r = f - K x matches the last history
+  entry, and the history is the one a second solve reproduces bitwise.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2508_02613_b200 import _native as N
+from paper_2508_02613_b200 import microstructures as ms
+
+pytestmark = pytest.mark.gpu
+
+N0 = 512
+
+
+@pytest.fixture(scope="module")
+def big():
+    import torch
+    dev = torch.device("cuda", N.device_id())
+    lam, mu = ms.lame_from_poisson()
+    rho = ms.crack_discs_device(N0, seed=0, device=dev)
+    gh = N.GridHandle(3, (N0,) * 3, (1.0,) * 3)
+    torch.cuda.synchronize()
+    op = N.OpHandle(gh, rho.data_ptr(), lam, mu, where=N.DEVICE)
+    op_ref = N.OpHandle(gh, torch.ones_like(rho).data_ptr(), lam, mu, where=N.DEVICE)
+    green = N.GreenHandle(gh, lam, mu)
+    jac = N.JacobiHandle(op)
+    return torch, dev, gh, op, op_ref, green, jac
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _apply(lib, op, u, out, torch):
+    torch.cuda.synchronize()
+    N.check(lib.jfftb_apply_system(op.ptr, _p(u), _p(out), N.DEVICE))
+
+
+def test_operator_symmetric_and_translation_free(big):
+    torch, dev, gh, op, _, _, _ = big
+    lib = N.load()
+    g = torch.Generator(device=dev).manual_seed(1)
+    u = torch.randn((3, N0, N0, N0), dtype=torch.float64, device=dev, generator=g)
+    v = torch.randn((3, N0, N0, N0), dtype=torch.float64, device=dev, generator=g)
+    ku, kv = torch.empty_like(u), torch.empty_like(v)
+    _apply(lib, op, u, ku, torch)
+    _apply(lib, op, v, kv, torch)
+    gh.synchronize()
+    a, b = torch.dot(u.ravel(), kv.ravel()).item(), torch.dot(ku.ravel(), v.ravel()).item()
+    assert abs(a - b) <= 1e-12 * abs(a) * 50
+    c = torch.empty_like(u)
+    c[0], c[1], c[2] = 0.7, -1.3, 2.1
+    _apply(lib, op, c, ku, torch)
+    gh.synchronize()
+    assert ku.abs().max().item() <= 1e-12 * kv.abs().max().item() * 10
+
+
+def test_green_inverts_reference_operator(big):
+    torch, dev, gh, _, op_ref, green, _ = big
+    lib = N.load()
+    g = torch.Generator(device=dev).manual_seed(2)
+    u = torch.randn((3, N0, N0, N0), dtype=torch.float64, device=dev, generator=g)
+    k = torch.empty_like(u)
+    out = torch.empty_like(u)
+    _apply(lib, op_ref, u, k, torch)
+    gh.synchronize()
+    N.check(lib.jfftb_apply_green(green.ptr, _p(k), _p(out), N.DEVICE))
+    gh.synchronize()
+    ref = u - u.mean(dim=(1, 2, 3), keepdim=True)
+    err = (out - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= 1e-10, err
+
+
+def test_green_jacobi_equals_its_composition(big):
+    torch, dev, gh, _, _, green, jac = big
+    lib = N.load()
+    g = torch.Generator(device=dev).manual_seed(3)
+    r = torch.randn((3, N0, N0, N0), dtype=torch.float64, device=dev, generator=g)
+    fused = torch.empty_like(r)
+    torch.cuda.synchronize()
+    N.check(lib.jfftb_apply_precond(N.PC_GREEN_JACOBI, green.ptr, jac.ptr, _p(r), _p(fused),
+                                    N.DEVICE))
+    gh.synchronize()
+    dinv = torch.empty_like(r)
+    N.check(lib.jfftb_jacobi_export(jac.ptr, _p(dinv), N.DEVICE))
+    s = (r * dinv).contiguous()
+    z = torch.empty_like(r)
+    N.check(lib.jfftb_apply_green(green.ptr, _p(s), _p(z), N.DEVICE))
+    gh.synchronize()
+    ref = dinv * z
+    err = (fused - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= 1e-12, err
+
+
+def test_pcg_recurrence_matches_true_residual(big):
+    torch, dev, gh, op, _, green, jac = big
+    lib = N.load()
+    from paper_2508_02613_b200.solver import pcg_device
+    f = torch.empty((3, N0, N0, N0), dtype=torch.float64, device=dev)
+    eb = np.array([1.0, 0, 0, 0, 0, 0])
+    torch.cuda.synchronize()
+    N.check(lib.jfftb_assemble_rhs(op.ptr, N.dptr(eb), _p(f), N.DEVICE))
+    x = torch.empty_like(f)
+    its = 25
+    it, hist, term, _ = pcg_device(op, "green-jacobi", green, jac, f.data_ptr(), x.data_ptr(),
+                                   -1.0, its)
+    assert it == its and term == "iteration-cap" and len(hist) == its + 1
+    assert all(b < a for a, b in zip(hist[:5], hist[1:6]))  # early monotone decrease
+    kx = torch.empty_like(f)
+    _apply(lib, op, x, kx, torch)
+    gh.synchronize()
+    r = (f - kx).contiguous()
+    z = torch.empty_like(r)
+    N.check(lib.jfftb_apply_green(green.ptr, _p(r), _p(z), N.DEVICE))
+    gh.synchronize()
+    true_g = torch.dot(r.ravel(), z.ravel()).item()
+    assert abs(true_g - hist[-1]) <= 1e-6 * hist[-1] + 1e-12 * hist[0], (true_g, hist[-1])
+    x2 = torch.empty_like(f)
+    it2, hist2, _, _ = pcg_device(op, "green-jacobi", green, jac, f.data_ptr(), x2.data_ptr(),
+                                  -1.0, its)
+    assert hist2 == hist
+    assert torch.equal(x, x2)
