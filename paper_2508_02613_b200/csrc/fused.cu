@@ -407,6 +407,11 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     else
       cta_fft_io<L, NQ, NT, false, false, CPAD, true, false>(sbuf, 1, RL, tw, spec + rbase,
                                                              nullptr, g.CS, 1);
+#ifndef JF_NO_PREFETCH
+    // the next row-set's rows into L2 while this one is solved and inverted
+    if (threadIdx.x < NQ && row + gridDim.x < rows)
+      bulk_prefetch_l2(spec + threadIdx.x * g.CS + (row + gridDim.x) * L, L * sizeof(double2));
+#endif
     if (GS) mbar_wait(&gbar, gphase);  // this row-set's Green planes
     gphase ^= 1;
     __syncthreads();
