@@ -247,7 +247,7 @@ void precond_device(int kind, jfftb_green* green, jfftb_jacobi* jac, jfftb_grid*
     if (kind == JFFTB_PC_GREEN_JACOBI) need_jac();
     if (g->fused) {
       DevBuf spec(sizeof(double2) * geo.d * spec_elems(g));
-      fused_precond_apply(geo, s, green->blocks,
+      fused_precond_apply(geo, s, green,
                           kind == JFFTB_PC_GREEN_JACOBI ? jac->inv_sqrt : nullptr, r, out,
                           spec.as<double2>(), g->twiddle);
       JF_CUDA(cudaStreamSynchronize(s));  // spec is freed on return
@@ -973,7 +973,7 @@ int jfftb_debug_fused_apply(jfftb_green* green, jfftb_jacobi* jac, int upto, con
     DevBuf din(sizeof(double) * n), dout(sizeof(double) * n),
         spec(sizeof(double2) * geo.d * ns);
     JF_CUDA(cudaMemcpyAsync(din.ptr, r, sizeof(double) * n, cudaMemcpyHostToDevice, g->stream));
-    fused_debug_apply(geo, g->stream, green->blocks, jac ? jac->inv_sqrt : nullptr,
+    fused_debug_apply(geo, g->stream, green, jac ? jac->inv_sqrt : nullptr,
                       din.as<double>(), dout.as<double>(), spec.as<double2>(), g->twiddle, upto);
     if (upto >= 5)
       JF_CUDA(cudaMemcpyAsync(out, dout.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost,

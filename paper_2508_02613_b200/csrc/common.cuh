@@ -372,7 +372,7 @@ inline int64_t spec_elems(const jfftb_grid* g) {
   return g->fused ? fused_spec_elems(g->geo) : g->geo.Nh;
 }
 void launch_twiddles(cudaStream_t s, double2* tw);
-void fused_precond_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
+void fused_precond_apply(const Geom& geo, cudaStream_t s, const jfftb_green* green,
                          const double* dinv, const double* r, double* out, double2* spec,
                          const double2* tw);
 enum { FUSED_APPLY = 0, FUSED_INIT = 1, FUSED_ITER = 2 };
@@ -382,13 +382,13 @@ void fused_stage_A(const Geom& geo, cudaStream_t s, int F, int mode, const PcgSt
 void fused_stage_B(const Geom& geo, cudaStream_t s, bool inv, const PcgState* st,
                    double2* spec, int ncomp, const double2* tw);
 int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const PcgState* st,
-                  const double* gpc, const double* gterm, double2* spec, double* partials,
-                  const double2* tw);
+                  const jfftb_green* gpc, const jfftb_green* gterm, double2* spec,
+                  double* partials, const double2* tw);
 void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                    const double2* zspec, const double* dinv, double* p, double* x,
                    const double2* tw);
 int64_t fused_component_stride(const Geom& geo);
-void fused_debug_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
+void fused_debug_apply(const Geom& geo, cudaStream_t s, const jfftb_green* green,
                        const double* dinv, const double* r, double* out, double2* spec,
                        const double2* tw, int upto);
 

@@ -332,6 +332,103 @@ __device__ __forceinline__ double hb_apply(const HB<D>& B, const double2 (&s)[D]
   return q;
 }
 
+// ---------------------------------------------------------------------------
+// Analytic Green blocks (3-D).  For the P1 Kuhn split the reference
+// operator's symbol is, with E_a = e^{i q_a}, D_a = E_a - 1, h_a = 1/dx_a,
+// w = prod(dx)/6 and P_ab = sum_t e^{i q.(o_tb - o_ta)} over the 6 simplices
+// (o_ta: low node of simplex t's edge along axis a, common.cuh edge_base),
+//   K_aa = 6 w ((lam + mu) h_a^2 |D_a|^2 + mu sum_c h_c^2 |D_c|^2)
+//   K_ab = w h_a h_b (lam conj(D_a) D_b P_ab + mu D_a conj(D_b) conj(P_ab))
+// (checked against the impulse-response transform of assemble_green,
+// preconditioners.py:50-80, to 4e-16 of its scale).  Every block but the DC
+// one is nonsingular (a nonzero q leaves some edge difference nonzero), so
+// the pseudo-inverse with the 1e-12 eigenvalue cutoff is the inverse, taken
+// here by cofactors; DC stays 0.  Pass C evaluates this per frequency instead
+// of streaming 4.5 U of stored Green planes: per row-set the q0 / q1 parts
+// are folded into a few constants, per frequency it costs ~150 flops.
+// ---------------------------------------------------------------------------
+struct GreenAna {
+  double lam, mu, w, h[3];
+};
+__device__ __forceinline__ double2 cpow1(double2 e, int v) {
+  return v > 0 ? e : (v < 0 ? cconj(e) : make_double2(1.0, 0.0));
+}
+constexpr int edge_bit(int t, int a, int c) { return (edge_base(3, t, a) >> c) & 1; }
+struct GRow {
+  double2 c01, d01, c02, d02, c12, d12;
+  double2 A[3][3];  // pair (01, 02, 12) x v2 + 1
+  double r0, r1;
+};
+__device__ __forceinline__ GRow green_row(const GreenAna& ga, double2 E0, double2 E1) {
+  GRow R;
+  const double2 D0 = make_double2(E0.x - 1.0, E0.y), D1 = make_double2(E1.x - 1.0, E1.y);
+  R.r0 = ga.h[0] * ga.h[0] * (D0.x * D0.x + D0.y * D0.y);
+  R.r1 = ga.h[1] * ga.h[1] * (D1.x * D1.x + D1.y * D1.y);
+  const double l01 = ga.w * ga.h[0] * ga.h[1], l02 = ga.w * ga.h[0] * ga.h[2],
+               l12 = ga.w * ga.h[1] * ga.h[2];
+  R.c01 = cscale(cmul(cconj(D0), D1), ga.lam * l01);
+  R.d01 = cscale(cmul(D0, cconj(D1)), ga.mu * l01);
+  R.c02 = cscale(cconj(D0), ga.lam * l02);
+  R.d02 = cscale(D0, ga.mu * l02);
+  R.c12 = cscale(cconj(D1), ga.lam * l12);
+  R.d12 = cscale(D1, ga.mu * l12);
+#pragma unroll
+  for (int pr = 0; pr < 3; ++pr)
+#pragma unroll
+    for (int v = 0; v < 3; ++v) R.A[pr][v] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int pr = 0; pr < 3; ++pr) {
+    const int a = pr == 2 ? 1 : 0, b = pr == 0 ? 1 : 2;
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      const int v0 = edge_bit(t, b, 0) - edge_bit(t, a, 0);
+      const int v1 = edge_bit(t, b, 1) - edge_bit(t, a, 1);
+      const int v2 = edge_bit(t, b, 2) - edge_bit(t, a, 2);
+      R.A[pr][v2 + 1] = cadd(R.A[pr][v2 + 1], cmul(cpow1(E0, v0), cpow1(E1, v1)));
+    }
+  }
+  return R;
+}
+__device__ __forceinline__ HB<3> green_block(const GreenAna& ga, const GRow& R, double2 E2,
+                                             bool dc) {
+  HB<3> B;
+  if (dc) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) B.dg[k] = B.re[k] = B.im[k] = 0.0;
+    return B;
+  }
+  const double2 D2 = make_double2(E2.x - 1.0, E2.y);
+  const double r2 = ga.h[2] * ga.h[2] * (D2.x * D2.x + D2.y * D2.y);
+  const double S = R.r0 + R.r1 + r2, lm = ga.lam + ga.mu, w6 = 6.0 * ga.w;
+  const double ka = w6 * (lm * R.r0 + ga.mu * S);
+  const double kd = w6 * (lm * R.r1 + ga.mu * S);
+  const double kf = w6 * (lm * r2 + ga.mu * S);
+  const double2 E2c = cconj(E2);
+  auto P = [&](int pr) {
+    return cadd(cadd(cmul(R.A[pr][0], E2c), R.A[pr][1]), cmul(R.A[pr][2], E2));
+  };
+  const double2 P01 = P(0), T02 = cmul(D2, P(1)), T12 = cmul(D2, P(2));
+  const double2 kb = cadd(cmul(R.c01, P01), cmul(R.d01, cconj(P01)));
+  const double2 kc = cadd(cmul(R.c02, T02), cmul(R.d02, cconj(T02)));
+  const double2 ke = cadd(cmul(R.c12, T12), cmul(R.d12, cconj(T12)));
+  const double nb = kb.x * kb.x + kb.y * kb.y, nc = kc.x * kc.x + kc.y * kc.y,
+               ne = ke.x * ke.x + ke.y * ke.y;
+  const double A0 = kd * kf - ne, A1 = ka * kf - nc, A2 = ka * kd - nb;
+  const double2 bec = cmul(cmul(kb, ke), cconj(kc));
+  const double det = ka * A0 - kd * nc - kf * nb + 2.0 * bec.x;
+  const double id = 1.0 / det;
+  B.dg[0] = A0 * id;
+  B.dg[1] = A1 * id;
+  B.dg[2] = A2 * id;
+  const double2 g01 = cscale(csub(cmul(kc, cconj(ke)), cscale(kb, kf)), id);
+  const double2 g02 = cscale(csub(cmul(kb, ke), cscale(kc, kd)), id);
+  const double2 g12 = cscale(csub(cmul(kc, cconj(kb)), cscale(ke, ka)), id);
+  B.re[0] = g01.x; B.im[0] = g01.y;
+  B.re[1] = g02.x; B.im[1] = g02.y;
+  B.re[2] = g12.x; B.im[2] = g12.y;
+  return B;
+}
+
 // Two CTAs per SM, two radix-8 butterflies per thread per stage.  The rows
 // never take a staging trip through shared memory: the first forward stage
 // reads its butterfly inputs straight from global memory (coalesced: thread j
@@ -343,25 +440,32 @@ constexpr int CPAD = 8;  // one padding slot every 8 elements of a row
 // Green planes staged in smem (GS) or read straight from global in the solve
 // (measured at 512^3: staged 3.69 ms, direct 4.19 ms)
 constexpr bool kGStage = true;
-constexpr int passC_gp(int D, bool GS) { return GS ? (D == 2 ? 4 : 9) : 0; }
+// GS: 0 Green planes read from global in the solve, 1 bulk-staged in shared
+// memory, 2 evaluated analytically (3-D, green_block)
+constexpr int passC_gp(int D, int GS) { return GS == 1 ? (D == 2 ? 4 : 9) : 0; }
 constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / 16); }
-constexpr int passC_bufd(int D, int L, int F, bool GS = true) {
+constexpr int passC_bufd(int D, int L, int F, int GS = 1) {
   return F * D * padded_len<CPAD>(L) * 2 + passC_gp(D, GS) * L;
 }
 // resident CTAs per SM the launch bounds aim for (capped by shared memory).
 // Double buffering the rows (next row-set in flight during this one's
 // transforms) was measured slower at 512^3 (6.6 ms vs 5.7 ms): it halves the
 // resident CTAs.
-constexpr int passC_minb(int D, int L, int F, bool GS = true) {
-  return passC_bufd(D, L, F, GS) * 8 <= 72 * 1024 ? 3
+#ifndef JF_CA_MINB
+#define JF_CA_MINB 2
+#endif
+constexpr int passC_minb(int D, int L, int F, int GS = 1) {
+  return GS == 2 ? JF_CA_MINB
+                 : passC_bufd(D, L, F, GS) * 8 <= 72 * 1024 ? 3
                                                    : (passC_bufd(D, L, F, GS) * 8 <= 110 * 1024 ? 2 : 1);
 }
 
-template <int D, int L, int F, int MODE, bool GS, bool IP>
+template <int D, int L, int F, int MODE, int GS, bool IP>
 __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     passC(FGeom g, const PcgState* __restrict__ st, const double* __restrict__ gpc,
           const double* __restrict__ gterm, double2* __restrict__ spec,
-          double* __restrict__ partials, const double2* __restrict__ tw) {
+          double* __restrict__ partials, const double2* __restrict__ tw, GreenAna ga) {
+  static_assert(GS != 2 || D == 3, "analytic Green blocks are 3-D");
   constexpr int NQ = F * D;  // rows held per frequency row
   constexpr int NT = passC_nt(D, L, F);
   constexpr int RL = padded_len<CPAD>(L);
@@ -383,10 +487,10 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
   // bulk copies issued by one thread and complete on gbar
   __shared__ uint64_t gbar;
   unsigned gphase = 0;
-  if (GS && threadIdx.x == 0) mbar_init(&gbar, 1);
+  if (GS == 1 && threadIdx.x == 0) mbar_init(&gbar, 1);
   __syncthreads();
   auto prefetch_green = [&](int64_t row) {
-    if (!GS || threadIdx.x != 0) return;
+    if (GS != 1 || threadIdx.x != 0) return;
     const int64_t rbase = row * L;
     fence_proxy_async();  // the previous row-set's reads of gsm come first
     mbar_expect_tx(&gbar, GP * L * sizeof(double));
@@ -412,14 +516,26 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     if (threadIdx.x < NQ && row + gridDim.x < rows)
       bulk_prefetch_l2(spec + threadIdx.x * g.CS + (row + gridDim.x) * L, L * sizeof(double2));
 #endif
-    if (GS) mbar_wait(&gbar, gphase);  // this row-set's Green planes
+    if (GS == 1) mbar_wait(&gbar, gphase);  // this row-set's Green planes
     gphase ^= 1;
     __syncthreads();
+    GRow grow;
+    bool dcrow = false;  // the row holding the zero frequency
+    if constexpr (GS == 2) {
+      const int k1 = (int)(row % (g.PS / L));
+      grow = green_row(ga, cconj(__ldg(tw + ((k0 * (kTwN / g.n0)) & (kTwN - 1)))),
+                       cconj(__ldg(tw + ((k1 * (kTwN / g.n1)) & (kTwN - 1)))));
+      dcrow = k0 == 0 && k1 == 0;
+    }
 #pragma unroll 1
     for (int k = threadIdx.x; k < L; k += NT) {
       const int64_t f = rbase + k;
       HB<D> B;
-      if constexpr (GS) {
+      if constexpr (GS == 2) {
+        const int k2 = IP ? dif_freq(L, k) : k;
+        B = green_block(ga, grow, cconj(__ldg(tw + ((k2 * (kTwN / L)) & (kTwN - 1)))),
+                        dcrow && k2 == 0);
+      } else if constexpr (GS == 1) {
 #pragma unroll
         for (int a = 0; a < D; ++a) B.dg[a] = gsm[a * L + k];
 #pragma unroll
@@ -651,12 +767,13 @@ void launchB_L(const FGeom& g, cudaStream_t s, const PcgState* st, double2* spec
   k<<<grid, NT, smem, s>>>(g, st, spec, comp0, g.nlast, tw);
   JF_LAUNCHED();
 }
-template <int D, int L, int F, int MODE>
-int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* gpc,
-              const double* gterm, double2* spec, double* partials, const double2* tw) {
+template <int D, int L, int F, int MODE, int GS, bool IP>
+int launchC_V(const FGeom& g, cudaStream_t s, const PcgState* st, const double* gpc,
+              const double* gterm, double2* spec, double* partials, const double2* tw,
+              const GreenAna& ga) {
   constexpr int NT = passC_nt(D, L, F);
-  const size_t smem = sizeof(double) * passC_bufd(D, L, F, kGStage);
-  auto k = fused_dif() ? passC<D, L, F, MODE, kGStage, true> : passC<D, L, F, MODE, kGStage, false>;
+  const size_t smem = sizeof(double) * passC_bufd(D, L, F, GS);
+  auto k = passC<D, L, F, MODE, GS, IP>;
   static int per_sm = -1;  // per instantiation
   if (per_sm < 0) {
     set_smem(k, smem);
@@ -664,9 +781,34 @@ int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* 
   }
   const int64_t rows = g.CS / L;
   const int blocks = (int)std::min<int64_t>(rows, (int64_t)std::max(per_sm, 1) * 148 * 4);
-  k<<<blocks, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw);
+  k<<<blocks, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, ga);
   JF_LAUNCHED();
   return blocks;
+}
+// JFFTB_GREEN_ANALYTIC=1 evaluates the 3-D Green blocks in pass C instead of
+// streaming the stored planes: 4.5 U less traffic and 36 KB less shared
+// memory per CTA, but measured slower at 512^3 (4.02 vs 3.34 ms: pass C is
+// bound by its shared-memory pipe and the ~150 extra flops per frequency
+// cost more than the Green reads) -- off by default; kept for grids where
+// the stored planes do not fit
+inline bool green_analytic_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("JFFTB_GREEN_ANALYTIC");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+template <int D, int L, int F, int MODE>
+int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* gpc,
+              const double* gterm, double2* spec, double* partials, const double2* tw,
+              const GreenAna& ga, bool analytic) {
+  if constexpr (D == 3) {
+    if (analytic && fused_dif())
+      return launchC_V<D, L, F, MODE, 2, true>(g, s, st, gpc, gterm, spec, partials, tw, ga);
+  }
+  if (fused_dif())
+    return launchC_V<D, L, F, MODE, 1, true>(g, s, st, gpc, gterm, spec, partials, tw, ga);
+  return launchC_V<D, L, F, MODE, 1, false>(g, s, st, gpc, gterm, spec, partials, tw, ga);
 }
 template <int M, int MODE>
 void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2* zspec,
@@ -720,17 +862,17 @@ void launchB(const FGeom& g, cudaStream_t s, bool inv, bool pred, const PcgState
 }
 int launchC(const FGeom& g, cudaStream_t s, int F, int mode, const PcgState* st,
             const double* gpc, const double* gterm, double2* spec, double* partials,
-            const double2* tw) {
+            const double2* tw, const GreenAna& ga, bool analytic) {
   const int nl = g.nlast;
   int blocks = 0;
   if (g.d == 3) {
-    if (mode == FM_APPLY) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 1, FM_APPLY>(g, s, st, gpc, gterm, spec, partials, tw))); }
-    else if (F == 2) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 2, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw))); }
-    else { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 1, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw))); }
+    if (mode == FM_APPLY) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 1, FM_APPLY>(g, s, st, gpc, gterm, spec, partials, tw, ga, analytic))); }
+    else if (F == 2) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 2, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw, ga, analytic))); }
+    else { JF_SIZE_SWITCH(nl, (blocks = launchC_L<3, LL, 1, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw, ga, analytic))); }
   } else {
-    if (mode == FM_APPLY) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 1, FM_APPLY>(g, s, st, gpc, gterm, spec, partials, tw))); }
-    else if (F == 2) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 2, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw))); }
-    else { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 1, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw))); }
+    if (mode == FM_APPLY) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 1, FM_APPLY>(g, s, st, gpc, gterm, spec, partials, tw, ga, analytic))); }
+    else if (F == 2) { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 2, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw, ga, analytic))); }
+    else { JF_SIZE_SWITCH(nl, (blocks = launchC_L<2, LL, 1, FM_ITER>(g, s, st, gpc, gterm, spec, partials, tw, ga, analytic))); }
   }
   return blocks;
 }
@@ -743,6 +885,20 @@ void launchI(const FGeom& g, cudaStream_t s, int mode, const PcgState* st, const
 }
 
 }  // namespace
+
+// analytic Green blocks for this green operator (and the termination one)?
+GreenAna green_ana(const Geom& geo, const jfftb_green* gpc) {
+  GreenAna ga{};
+  ga.lam = gpc->lambda_ref;
+  ga.mu = gpc->mu_ref;
+  ga.w = geo.w;
+  for (int a = 0; a < 3; ++a) ga.h[a] = geo.hinv[a];
+  return ga;
+}
+bool use_analytic(const Geom& geo, const jfftb_green* gpc, const jfftb_green* gterm) {
+  return geo.d == 3 && green_analytic_enabled() && gpc->slab_lo < 0 &&
+         gterm->lambda_ref == gpc->lambda_ref && gterm->mu_ref == gpc->mu_ref;
+}
 
 void launch_twiddles(cudaStream_t s, double2* tw) {
   twiddle_kernel<<<kTwN / 256, 256, 0, s>>>(tw);
@@ -771,25 +927,31 @@ int64_t fused_spec_elems(const Geom& g) { return (int64_t)(g.n[0] / 2 + 1) * (g.
 
 // apply the Green (dinv == null) or Green-Jacobi preconditioner through the
 // fused passes: out = D G D r  (spec: d * CS complex scratch)
-void fused_precond_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
+void fused_precond_apply(const Geom& geo, cudaStream_t s, const jfftb_green* green,
                          const double* dinv, const double* r, double* out, double2* spec,
                          const double2* tw) {
   const FGeom g = fgeom(geo);
+  const double* gblocks = green->blocks;
+  const GreenAna ga = green_ana(geo, green);
+  const bool an = use_analytic(geo, green, green);
   launchA(g, s, 1, FM_APPLY, nullptr, const_cast<double*>(r), nullptr, dinv, spec, tw);
   if (g.d == 3) launchB(g, s, false, false, nullptr, spec, 0, g.d, tw);
-  launchC(g, s, 1, FM_APPLY, nullptr, gblocks, gblocks, spec, nullptr, tw);
+  launchC(g, s, 1, FM_APPLY, nullptr, gblocks, gblocks, spec, nullptr, tw, ga, an);
   if (g.d == 3) launchB(g, s, true, false, nullptr, spec, 0, g.d, tw);
   launchI(g, s, FM_APPLY, nullptr, spec, dinv, nullptr, nullptr, out, tw);
 }
 
 // diagnostic: run the APPLY passes up to `upto` (1 A, 2 B, 3 C, 4 B', 5 I)
-void fused_debug_apply(const Geom& geo, cudaStream_t s, const double* gblocks,
+void fused_debug_apply(const Geom& geo, cudaStream_t s, const jfftb_green* green,
                        const double* dinv, const double* r, double* out, double2* spec,
                        const double2* tw, int upto) {
   const FGeom g = fgeom(geo);
+  const double* gblocks = green->blocks;
+  const GreenAna ga = green_ana(geo, green);
+  const bool an = use_analytic(geo, green, green);
   launchA(g, s, 1, FM_APPLY, nullptr, const_cast<double*>(r), nullptr, dinv, spec, tw);
   if (upto >= 2 && g.d == 3) launchB(g, s, false, false, nullptr, spec, 0, g.d, tw);
-  if (upto >= 3) launchC(g, s, 1, FM_APPLY, nullptr, gblocks, gblocks, spec, nullptr, tw);
+  if (upto >= 3) launchC(g, s, 1, FM_APPLY, nullptr, gblocks, gblocks, spec, nullptr, tw, ga, an);
   if (upto >= 4 && g.d == 3) launchB(g, s, true, false, nullptr, spec, 0, g.d, tw);
   if (upto >= 5) launchI(g, s, FM_APPLY, nullptr, spec, dinv, nullptr, nullptr, out, tw);
 }
@@ -809,19 +971,23 @@ void fused_stage_B(const Geom& geo, cudaStream_t s, bool inv, const PcgState* st
 }
 // returns the number of partial pairs written
 int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const PcgState* st,
-                  const double* gpc, const double* gterm, double2* spec, double* partials,
-                  const double2* tw) {
+                  const jfftb_green* gpc_h, const jfftb_green* gterm_h, double2* spec,
+                  double* partials, const double2* tw) {
   const FGeom g = fgeom(geo);
+  const double* gpc = gpc_h->blocks;
+  const double* gterm = gterm_h->blocks;
+  const GreenAna ga = green_ana(geo, gpc_h);
+  const bool an = use_analytic(geo, gpc_h, gterm_h);
   if (quad_only) {
     int blocks = 0;
     if (g.d == 3) {
-      JF_SIZE_SWITCH(g.nlast, (blocks = launchC_L<3, LL, 1, FM_QUAD>(g, s, st, gpc, gterm, spec, partials, tw)));
+      JF_SIZE_SWITCH(g.nlast, (blocks = launchC_L<3, LL, 1, FM_QUAD>(g, s, st, gpc, gterm, spec, partials, tw, ga, an)));
     } else {
-      JF_SIZE_SWITCH(g.nlast, (blocks = launchC_L<2, LL, 1, FM_QUAD>(g, s, st, gpc, gterm, spec, partials, tw)));
+      JF_SIZE_SWITCH(g.nlast, (blocks = launchC_L<2, LL, 1, FM_QUAD>(g, s, st, gpc, gterm, spec, partials, tw, ga, an)));
     }
     return blocks;
   }
-  return launchC(g, s, F, FM_ITER, st, gpc, gterm, spec, partials, tw);
+  return launchC(g, s, F, FM_ITER, st, gpc, gterm, spec, partials, tw, ga, an);
 }
 void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                    const double2* zspec, const double* dinv, double* p, double* x,

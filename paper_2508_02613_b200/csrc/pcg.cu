@@ -235,7 +235,7 @@ static void pcg_precond_phase_fused(jfftb_grid* g, jfftb_jacobi* jac, jfftb_gree
     if (!INIT) prof_mark(g);
     fused_stage_B(geo, s, false, B.st, B.spec, F * geo.d, tw);
     if (!INIT) prof_mark(g);
-    scount = fused_stage_C(geo, s, F, false, B.st, gpc->blocks, gterm->blocks, B.spec, B.spart, tw);
+    scount = fused_stage_C(geo, s, F, false, B.st, gpc, gterm, B.spec, B.spart, tw);
   } else {
     update_kernel<KIND, INIT><<<kRedBlocks, 256, 0, s>>>(n, B.st, B.x, r, B.p, B.kp, dinv, sz,
                                                          B.upart);
@@ -244,7 +244,7 @@ static void pcg_precond_phase_fused(jfftb_grid* g, jfftb_jacobi* jac, jfftb_gree
     fused_stage_A(geo, s, 1, FUSED_APPLY, B.st, r, nullptr, nullptr, B.spec, tw);
     fused_stage_B(geo, s, false, B.st, B.spec, geo.d, tw);
     if (!INIT) prof_mark(g);
-    scount = fused_stage_C(geo, s, 1, true, B.st, gterm->blocks, gterm->blocks, B.spec, B.spart, tw);
+    scount = fused_stage_C(geo, s, 1, true, B.st, gterm, gterm, B.spec, B.spart, tw);
   }
   if (!INIT) prof_mark(g);
   finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, scount, B.upart, kRedBlocks,

@@ -117,3 +117,35 @@ def floor_dev(rho, c, h, f, kind, bl, inv, x):
     finally:
         X._dot = orig
     return rel(x2, x)
+
+
+def test_analytic_green_blocks_match_stored():
+    """The closed-form 3-D Green blocks (JFFTB_GREEN_ANALYTIC=1, fused.cu
+    green_block) against the stored pseudo-inverse through a full fused
+    application, in a fresh process (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, sys.argv[1])
+from oracle import jfft_oracle as X
+from paper_2508_02613_b200 import grid as G
+from paper_2508_02613_b200.material import isotropic_material
+from paper_2508_02613_b200.preconditioners import apply_green, assemble_green
+n, lengths = 32, (1.0, 2.0, 0.5)
+grid = G.make_grid(n, lengths)
+mat = isotropic_material(0.7, 0.4, 3)
+green = assemble_green(grid, mat)
+u = np.random.default_rng(4).normal(size=(3, n, n, n))
+out = apply_green(green, G.VectorField(grid, u)).values
+ref = X.apply_green(X.assemble_green((n,) * 3, lengths, X.isotropic_stiffness(3, 0.7, 0.4)), u)
+err = np.abs(out - ref).max() / np.abs(ref).max()
+assert err <= 1e-12, err
+print("ok", err)
+'''
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, JFFTB_GREEN_ANALYTIC="1")
+    r = subprocess.run([sys.executable, "-c", code, repo], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
