@@ -479,14 +479,31 @@ def run_e2e(args, P, torch, world):
                    "(pinned), solution returned on the host"}
 
 
+def _json_stdout():
+    """The driver reads exactly one JSON line from stdout.  Libraries may
+    print to file descriptor 1 (NCCL's version banner under torchrun), so fd 1
+    is pointed at stderr for the whole run and the result line goes to a
+    duplicate of the original stdout."""
+    sys.stdout.flush()
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    return out
+
+
+def _emit(out, line):
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
     args = parse()
+    out = _json_stdout()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         line = run_reference(args, rank)
         if line is not None:
-            print(json.dumps(line), flush=True)
+            _emit(out, line)
         return
     import torch
     import torch.distributed as dist
@@ -507,7 +524,7 @@ def main():
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline_single(args)
-        print(json.dumps(line), flush=True)
+        _emit(out, line)
     if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
