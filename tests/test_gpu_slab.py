@@ -56,3 +56,46 @@ def test_slab_device_matches_oracle(nccl_group, n, kind):
     assert np.abs(x2 - x).max() <= 1e-8 * np.abs(x).max()
     if solver.dinv is not None:
         assert np.abs(solver.dinv.cpu().numpy() - inv).max() <= 1e-14 * inv.max()
+
+
+def test_fused_and_slab_paths_agree_at_bench_size(nccl_group):
+    """BASELINE config 4 (512^3 crack discs, Green-Jacobi): the fused
+    single-GPU path (hand-written FFT passes, device PCG) and the slab driver
+    (cuFFT transforms, frequency-slab block solve, separate stencil launch
+    geometry) are independent implementations of the same recurrence.  No CPU
+    oracle fits at this size, so they check each other: identical iteration
+    count, histories and solutions to round-off."""
+    from paper_2508_02613_b200 import _native as N
+    from paper_2508_02613_b200 import microstructures as ms
+    from paper_2508_02613_b200.slab import DeviceBackend, SlabLayout, SlabPCG
+    from paper_2508_02613_b200.solver import pcg_device
+    n = (512, 512, 512)
+    dev = torch.device("cuda", 0)
+    lam, mu = ms.lame_from_poisson()
+    rho = ms.crack_discs_device(512, seed=0, device=dev)
+    eb = np.array([1.0, 0, 0, 0, 0, 0])
+    its = 12
+    lay = SlabLayout(n, (1.0,) * 3, 1, 0)
+    solver = SlabPCG(lay, DeviceBackend(dev), rho, lam, mu, kind="green-jacobi")
+    rhs = solver.assemble_rhs(eb)
+    it2, hist2, term2, x2, _ = solver.solve(rhs, eta=-1.0, max_iter=its)
+    x2 = x2.cpu().numpy()
+    del solver
+    torch.cuda.empty_cache()
+    gh = N.GridHandle(3, n, (1.0,) * 3)
+    torch.cuda.synchronize()
+    op = N.OpHandle(gh, rho.data_ptr(), lam, mu, where=N.DEVICE)
+    green = N.GreenHandle(gh, lam, mu)
+    jac = N.JacobiHandle(op)
+    f = torch.empty((3,) + n, dtype=torch.float64, device=dev)
+    import ctypes
+    N.check(N.load().jfftb_assemble_rhs(op.ptr, N.dptr(eb), ctypes.c_void_p(f.data_ptr()),
+                                        N.DEVICE))
+    x = torch.empty_like(f)
+    it, hist, term, _ = pcg_device(op, "green-jacobi", green, jac, f.data_ptr(), x.data_ptr(),
+                                   -1.0, its)
+    assert it == it2 == its and term == term2
+    h1, h2 = np.array(hist), np.array(hist2)
+    assert np.abs(h1 - h2).max() <= 1e-9 * h1[0], (h1, h2)
+    x = x.cpu().numpy()
+    assert np.abs(x - x2).max() <= 1e-8 * np.abs(x).max()
