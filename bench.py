@@ -37,6 +37,7 @@ WORKLOADS = {
     # name: (d, n, generator, eps_bar)
     "3d512": (3, 512, "cracks", [1.0, 0, 0, 0, 0, 0]),
     "3d128": (3, 128, "spheres", [1.0, 0, 0, 0, 0, 0]),
+    "3d256": (3, 256, "cracks", [1.0, 0, 0, 0, 0, 0]),
     "2d2048": (2, 2048, "bernoulli20", [0.0, 0.0, np.sqrt(2.0) * 0.5]),
 }
 
