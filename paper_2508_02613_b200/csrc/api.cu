@@ -226,6 +226,66 @@ PcgBuffers pcg_workspace(jfftb_grid* g, int kcount, int max_iter) {
   return B;
 }
 
+bool graphs_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("JFFTB_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+void drop_iteration_graph(jfftb_grid* g) {
+  if (g->iter_graph) cudaGraphExecDestroy(g->iter_graph);
+  g->iter_graph = nullptr;
+  g->iter_kind = -1;
+}
+
+// replay (capturing first if needed) one PCG iteration as a CUDA graph; the
+// graph bakes in every pointer of the iteration, so it is keyed on them
+void run_iteration_graph(jfftb_grid* g, int kind, jfftb_op* op, jfftb_jacobi* jac,
+                         jfftb_green* gpc, jfftb_green* gterm, const PcgBuffers& B) {
+  constexpr int kIterKey = jfftb_grid::kIterKey;
+  const void* key[kIterKey] = {op, op->rho, jac, jac ? jac->inv_sqrt : nullptr, gpc->blocks,
+                               gterm->blocks, B.x, B.st, B.hist, g->stream};
+  bool hit = g->iter_graph != nullptr && g->iter_kind == kind &&
+             g->iter_lame[0] == op->lambda0 && g->iter_lame[1] == op->mu0;
+  for (int i = 0; hit && i < kIterKey; ++i) hit = g->iter_key[i] == key[i];
+  if (!hit) {
+    drop_iteration_graph(g);
+    cudaGraph_t graph = nullptr;
+    const int64_t before = g_launches;
+    // capture on the grid's own stream (the caller's may be the legacy
+    // default stream, which cannot be captured); the graph is launched on
+    // the caller's stream below
+    cudaStream_t user = g->stream;
+    JF_CUDA(cudaStreamSynchronize(user));
+    g->stream = g->own_stream;
+    JF_CUDA(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      pcg_dispatch(kind, false, op, jac, gpc, gterm, B);
+    } catch (...) {
+      cudaStreamEndCapture(g->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      g->stream = user;
+      throw;
+    }
+    const cudaError_t ec = cudaStreamEndCapture(g->stream, &graph);
+    g->stream = user;
+    JF_CUDA(ec);
+    g->iter_launches = (int)(g_launches - before);
+    g_launches = before;
+    const cudaError_t e = cudaGraphInstantiate(&g->iter_graph, graph, 0);
+    cudaGraphDestroy(graph);
+    JF_CUDA(e);
+    for (int i = 0; i < kIterKey; ++i) g->iter_key[i] = key[i];
+    g->iter_kind = kind;
+    g->iter_lame[0] = op->lambda0;
+    g->iter_lame[1] = op->mu0;
+  }
+  JF_CUDA(cudaGraphLaunch(g->iter_graph, g->stream));
+  count_launch(g->iter_launches);
+}
+
 // precondition r (device, d*N) into out (device) for kind (-1 = jacobi half)
 void precond_device(int kind, jfftb_green* green, jfftb_jacobi* jac, jfftb_grid* g,
                     const double* r, double* out) {
@@ -410,6 +470,7 @@ void grid_free(jfftb_grid* g) {
     if (g->ws_host) cudaFreeHost(g->ws_host);
     if (g->twiddle) cudaFree(g->twiddle);
     free_host_staging(g);
+    drop_iteration_graph(g);
     prof_collect(g, 0, true);
     for (auto e : g->ev_free) cudaEventDestroy(e);
     cudaStreamDestroy(g->own_stream);
@@ -928,8 +989,20 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     // host loop: iterations are predicated on the device flag, so a few can
     // be queued ahead of each poll; the batch grows while the solve runs
     int batch = 1;
+    // After the first (uncaptured) iteration, further iterations replay one
+    // captured CUDA graph: one launch instead of ~10 and shorter gaps between
+    // the kernels.  Not while the stage profiler records events.
+    const bool graphs = g->fused && !g->prof && graphs_enabled();
+    bool first = true;
     while (!done) {
-      for (int k = 0; k < batch; ++k) pcg_dispatch(kind, false, op, jac, green_pc, green_term, B);
+      for (int k = 0; k < batch; ++k) {
+        if (graphs && !first) {
+          run_iteration_graph(g, kind, op, jac, green_pc, green_term, B);
+        } else {
+          pcg_dispatch(kind, false, op, jac, green_pc, green_term, B);
+        }
+        first = false;
+      }
       done = poll();
       prof_collect(g, hs->iters, false);
       batch = std::min(batch * 2, 8);

@@ -89,6 +89,14 @@ struct jfftb_grid {
   bool plans_ready = false;
   void* fft_work = nullptr;
   void* host_stage = nullptr;   // pinned staging ring for pageable host copies (hostio.cu)
+  // one PCG iteration captured as a CUDA graph (api.cu jfftb_pcg), valid for
+  // the key it was captured with
+  static constexpr int kIterKey = 10;
+  cudaGraphExec_t iter_graph = nullptr;
+  const void* iter_key[kIterKey] = {};
+  double iter_lame[2] = {0.0, 0.0};
+  int iter_kind = -1;
+  int iter_launches = 0;
   size_t fft_work_bytes = 0;
   // reduction scratch
   double* partials = nullptr;   // per-block partial sums
