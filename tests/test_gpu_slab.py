@@ -99,3 +99,40 @@ def test_fused_and_slab_paths_agree_at_bench_size(nccl_group):
     assert np.abs(h1 - h2).max() <= 1e-9 * h1[0], (h1, h2)
     x = x.cpu().numpy()
     assert np.abs(x - x2).max() <= 1e-8 * np.abs(x).max()
+
+
+def test_fused_and_slab_converge_alike_at_bench_size(nccl_group):
+    """The same cross-check on a converged BASELINE config-4 solve
+    (eta = 1e-6 on <r, G r>, reference semantics): iteration counts within the
+    +-1 the BASELINE allows (observed equal), solutions to round-off."""
+    import ctypes
+    from paper_2508_02613_b200 import _native as N
+    from paper_2508_02613_b200 import microstructures as ms
+    from paper_2508_02613_b200.slab import DeviceBackend, SlabLayout, SlabPCG
+    from paper_2508_02613_b200.solver import pcg_device
+    n = (512, 512, 512)
+    dev = torch.device("cuda", 0)
+    lam, mu = ms.lame_from_poisson()
+    rho = ms.crack_discs_device(512, seed=0, device=dev)
+    eb = np.array([1.0, 0, 0, 0, 0, 0])
+    gh = N.GridHandle(3, n, (1.0,) * 3)
+    torch.cuda.synchronize()
+    op = N.OpHandle(gh, rho.data_ptr(), lam, mu, where=N.DEVICE)
+    green = N.GreenHandle(gh, lam, mu)
+    jac = N.JacobiHandle(op)
+    f = torch.empty((3,) + n, dtype=torch.float64, device=dev)
+    N.check(N.load().jfftb_assemble_rhs(op.ptr, N.dptr(eb), ctypes.c_void_p(f.data_ptr()),
+                                        N.DEVICE))
+    x = torch.empty_like(f)
+    it, hist, term, _ = pcg_device(op, "green-jacobi", green, jac, f.data_ptr(), x.data_ptr(),
+                                   1e-6, 999)
+    x = x.cpu().numpy()
+    del op, green, jac, f
+    torch.cuda.empty_cache()
+    assert term == "converged" and it > 5
+    lay = SlabLayout(n, (1.0,) * 3, 1, 0)
+    solver = SlabPCG(lay, DeviceBackend(dev), rho, lam, mu, kind="green-jacobi")
+    it2, hist2, term2, x2, _ = solver.solve(solver.assemble_rhs(eb), eta=1e-6)
+    assert term2 == "converged" and abs(it2 - it) <= 1, (it, it2)
+    x2 = x2.cpu().numpy()
+    assert np.abs(x - x2).max() <= 1e-8 * np.abs(x).max()
