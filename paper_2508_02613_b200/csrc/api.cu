@@ -968,6 +968,10 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     PcgBuffers B = pcg_workspace(g, kcount, max_iter);
     PcgState* hs = g->ws_host;
 
+    // fault in a pageable solution array on host threads while the device
+    // iterates, so the final d2h is a plain staged memcpy
+    HostPrefault prefault(where == JFFTB_HOST ? x_out : nullptr, sizeof(double) * n);
+
     PcgState h0{};
     h0.eta = eta;
     h0.max_iter = max_iter;
@@ -1022,6 +1026,7 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     }
     *terminated = (hs->gnorm2 <= eta) ? JFFTB_CONVERGED : JFFTB_ITERATION_CAP;
     launch_sub_mean(geo, s, B.x, ensure_partials(g, kRedBlocks * 3 + 3));
+    prefault.wait();
     if (x_out) {
       if (where == JFFTB_HOST)
         copy_d2h(g, x_out, B.x, sizeof(double) * n, s);

@@ -9,6 +9,7 @@
 #include <stdexcept>
 #include <string>
 #include <atomic>
+#include <thread>
 #include <vector>
 
 #include "../../include/jfftb200.h"
@@ -313,6 +314,23 @@ bool fused_dif();
 void copy_h2d(jfftb_grid* g, void* dst, const void* src, size_t bytes, cudaStream_t s);
 void copy_d2h(jfftb_grid* g, void* dst, const void* src, size_t bytes, cudaStream_t s);
 void free_host_staging(jfftb_grid* g);
+
+// Page-faults a pageable host output array on a few host threads while the
+// device works (a fresh numpy array has no pages yet: the faults, not the
+// memcpy, dominate its staged d2h).  Contents are preserved (each page is
+// rewritten with its own first byte).  No-op for pinned or small arrays.
+// wait() joins the team; the destructor waits too.
+class HostPrefault {
+ public:
+  HostPrefault(void* p, size_t bytes);
+  ~HostPrefault() { wait(); }
+  void wait();
+  HostPrefault(const HostPrefault&) = delete;
+  HostPrefault& operator=(const HostPrefault&) = delete;
+
+ private:
+  std::vector<std::thread> team_;
+};
 
 // input generators (generators.cu)
 void launch_binomial_filter(const Geom& g, cudaStream_t s, double* field, double* scratch,

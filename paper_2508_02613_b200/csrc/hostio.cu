@@ -147,6 +147,30 @@ void copy_d2h(jfftb_grid* g, void* dst, const void* src, size_t bytes, cudaStrea
               true);
 }
 
+HostPrefault::HostPrefault(void* p, size_t bytes) {
+  if (!p || bytes < kChunk || is_pinned(p)) return;
+  // a quarter of the copy team: the faults finish well inside any solve long
+  // enough for them to matter, and the polling host thread keeps a core
+  const int nt = std::max(1, copy_threads() / 4);
+  constexpr size_t kPage = 4096;
+  char* base = static_cast<char*>(p);
+  for (int t = 0; t < nt; ++t) {
+    team_.emplace_back([=] {
+      size_t lo, hi;
+      slice(bytes, t, nt, lo, hi);
+      for (size_t o = (lo + kPage - 1) & ~(kPage - 1); o < hi; o += kPage) {
+        volatile char* q = base + o;
+        *q = *q;  // write fault, contents unchanged
+      }
+    });
+  }
+}
+
+void HostPrefault::wait() {
+  for (auto& th : team_) th.join();
+  team_.clear();
+}
+
 void free_host_staging(jfftb_grid* g) {
   if (!g->host_stage) return;
   auto* st = static_cast<Staging*>(g->host_stage);
