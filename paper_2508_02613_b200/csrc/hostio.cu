@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <system_error>
 #include <thread>
 #include <vector>
 
@@ -117,7 +118,15 @@ void staged_copy(jfftb_grid* g, char* host, char* dev, size_t bytes, cudaStream_
   };
   std::vector<std::thread> team;
   team.reserve(nt - 1);
-  for (int t = 1; t < nt; ++t) team.emplace_back(worker, t);
+  try {
+    for (int t = 1; t < nt; ++t) team.emplace_back(worker, t);
+  } catch (const std::system_error&) {
+    // the started workers would wait for the missing ones: stop them
+    err.store(cudaErrorMemoryAllocation);
+    for (auto& th : team) th.join();
+    JF_CUDA(cudaStreamSynchronize(s));
+    throw Error(JFFTB_ECUDA, "staged host copy: cannot start the copy threads");
+  }
   worker(0);
   for (auto& th : team) th.join();
   if (err.load() != cudaSuccess)
@@ -154,15 +163,19 @@ HostPrefault::HostPrefault(void* p, size_t bytes) {
   const int nt = std::max(1, copy_threads() / 4);
   constexpr size_t kPage = 4096;
   char* base = static_cast<char*>(p);
-  for (int t = 0; t < nt; ++t) {
-    team_.emplace_back([=] {
-      size_t lo, hi;
-      slice(bytes, t, nt, lo, hi);
-      for (size_t o = (lo + kPage - 1) & ~(kPage - 1); o < hi; o += kPage) {
-        volatile char* q = base + o;
-        *q = *q;  // write fault, contents unchanged
-      }
-    });
+  auto touch = [=](int t) {
+    size_t lo, hi;
+    slice(bytes, t, nt, lo, hi);
+    for (size_t o = (lo + kPage - 1) & ~(kPage - 1); o < hi; o += kPage) {
+      volatile char* q = base + o;
+      *q = *q;  // write fault, contents unchanged
+    }
+  };
+  // the prefault is an optimisation: if a thread cannot be started, the
+  // slices already handed out still run and the rest are left to the copy
+  try {
+    for (int t = 0; t < nt; ++t) team_.emplace_back(touch, t);
+  } catch (const std::system_error&) {
   }
 }
 
