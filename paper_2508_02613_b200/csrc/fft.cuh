@@ -413,6 +413,17 @@ __device__ __forceinline__ void cta_fft_dif_qf(double2* buf, int ks, const doubl
   }
 }
 
+// stages S .. END-1 of cta_fft_dif_qf (the caller fuses the rest)
+template <int L, int NSEQ, int NT, int S, int END>
+__device__ __forceinline__ void cta_fft_dif_qf_until(double2* buf, int ks,
+                                                     const double2* __restrict__ tw) {
+  if constexpr (S < END) {
+    cta_fft_ip_stage<L, NSEQ, NT, false, 0, S, false, false, true>(buf, 0, tw, nullptr, nullptr, 0,
+                                                                   ks);
+    cta_fft_dif_qf_until<L, NSEQ, NT, S + 1, END>(buf, ks, tw);
+  }
+}
+
 template <int L, int NSEQ, int NT, int PAD, bool GOUT, int S = fft_nstages(L) - 1>
 __device__ __forceinline__ void cta_fft_dit_inv(double2* buf, int qs,
                                                 const double2* __restrict__ tw, double2* gout,

@@ -177,7 +177,7 @@ constexpr int passA3_nt() { return tw_a(M) * (M / fft_radix(M, 0)); }
 template <int M>
 constexpr bool passA3_ok() { return passA3_nt<M>() >= 64 && passA3_nt<M>() <= 1024; }
 
-template <int M, int MODE>
+template <int M, int MODE, bool FL>
 __global__ void __launch_bounds__(passA3_nt<M>(), 1)
     passA3(FGeom g, const PcgState* __restrict__ st, double* __restrict__ r,
            const double* __restrict__ kp, const double* __restrict__ dinv,
@@ -239,8 +239,6 @@ __global__ void __launch_bounds__(passA3_nt<M>(), 1)
     sbuf[(j + Q0 * t) * FTW + TW + col] = v1[t];
   }
   __syncthreads();
-  cta_fft_dif_qf<M, FTW, NT, 1>(sbuf, FTW, tw);
-  // unpack X[k], k = 0..M, pairwise (k, M - k) from the digit-reversed slots
   constexpr int TWS = kTwN / (2 * M);
   auto unpack = [&](double2 zk, double2 zc, int k) {
     const double2 fe = cscale(cadd(zk, zc), 0.5);
@@ -248,6 +246,53 @@ __global__ void __launch_bounds__(passA3_nt<M>(), 1)
     const double2 w = __ldg(tw + ((k * TWS) & (kTwN - 1)));         // e^{-2 pi i k / n0}
     return cadd(fe, cmul(w, mul_mi<false>(fo)));                    // Fe + w Fo
   };
+  if constexpr (FL) {
+    // last DIF stage (unit stride: butterfly b owns slots RL b .. RL b + RL-1)
+    // fused with the unpack.  The mirror frequencies (M - k) mod M of one
+    // butterfly all sit in one partner butterfly bp, so a thread transforms
+    // the pair (b, bp) in registers and emits every X[k], X[M - k] they
+    // hold: two shared-memory passes (last-stage write, unpack read) fewer.
+    constexpr int NS = fft_nstages(M);
+    constexpr int RL = fft_radix(M, NS - 1);
+    static_assert(fft_span(M, NS - 1) == RL, "last DIF stage has unit stride");
+    cta_fft_dif_qf_until<M, FTW, NT, 1, NS - 1>(sbuf, FTW, tw);
+    constexpr int NB = M / RL;
+    for (int e = threadIdx.x; e < NB * FTW; e += NT) {
+      const int b = e / FTW, q = e % FTW;  // warp-uniform b
+      const int bp = dif_pos(M, (M - dif_freq(M, RL * b)) % M) / RL;
+      if (bp < b) continue;
+      double2 u[8], w[8];  // dftR works on 8-slot arrays
+#pragma unroll
+      for (int t = 0; t < RL; ++t) {
+        u[t] = sbuf[(RL * b + t) * FTW + q];
+        w[t] = sbuf[(RL * bp + t) * FTW + q];
+      }
+      dftR<RL, false>(u);
+      dftR<RL, false>(w);
+      const int f = q / TW, cl = q % TW;
+      double2* out = spec + (f * g.d + c) * g.CS + col0 + cl;
+      auto emit = [&](const double2 (&x)[8], const double2 (&y)[8], int bx, int by) {
+#pragma unroll
+        for (int t = 0; t < RL; ++t) {
+          const int k = dif_freq(M, RL * bx + t);
+          if (2 * k > M) continue;
+          const int kc = M - k;
+          const int tp = dif_pos(M, kc % M) - RL * by;
+          double2 zb = y[0];
+#pragma unroll
+          for (int s = 1; s < RL; ++s)
+            if (s == tp) zb = y[s];
+          out[(int64_t)k * g.PS] = unpack(x[t], cconj(zb), k);
+          if (kc != k) out[(int64_t)kc * g.PS] = unpack(zb, cconj(x[t]), kc);
+        }
+      };
+      emit(u, w, b, bp);
+      if (bp != b) emit(w, u, bp, b);
+    }
+    return;
+  }
+  cta_fft_dif_qf<M, FTW, NT, 1>(sbuf, FTW, tw);
+  // unpack X[k], k = 0..M, pairwise (k, M - k) from the digit-reversed slots
   for (int e = threadIdx.x; e < (M / 2 + 1) * FTW; e += NT) {
     const int k = e / FTW, q = e % FTW;
     const int f = q / TW, cl = q % TW;
@@ -735,6 +780,14 @@ inline bool passA3_enabled() {
   }();
   return v;
 }
+// JFFTB_PASSA3_FL=0: last transform stage and unpack as separate smem passes
+inline bool passA3_fused_last() {
+  static const bool v = [] {
+    const char* e = std::getenv("JFFTB_PASSA3_FL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 template <int M, int F, int MODE>
 void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, const double* kp,
                const double* dinv, double2* spec, const double2* tw) {
@@ -743,7 +796,7 @@ void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, co
       constexpr int TW = tw_a(M);
       constexpr int NT = passA3_nt<M>();
       const size_t smem = sizeof(double2) * 2 * TW * M;
-      auto k = passA3<M, MODE>;
+      auto k = passA3_fused_last() ? passA3<M, MODE, true> : passA3<M, MODE, false>;
       static bool attr = false;
       if (!attr) { set_smem(k, smem); attr = true; }
       dim3 grid((unsigned)(g.PS / TW), g.d);
