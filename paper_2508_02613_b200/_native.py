@@ -242,13 +242,14 @@ class JacobiHandle(_Handle):
 _grid_cache: dict = {}
 
 
-def grid_handle(d: int, n, lengths) -> GridHandle:
-    """One grid context per (d, n, lengths, device) and process."""
-    key = (os.getpid(), d, tuple(int(k) for k in n), tuple(float(l) for l in lengths),
-           device_id())
+def grid_handle(d: int, n, lengths, device: int | None = None) -> GridHandle:
+    """One grid context per (d, n, lengths, device) and process; ``device``
+    defaults to JFFTB_DEVICE (the containers' device)."""
+    dev = device_id() if device is None else int(device)
+    key = (os.getpid(), d, tuple(int(k) for k in n), tuple(float(l) for l in lengths), dev)
     h = _grid_cache.get(key)
     if h is None:
-        h = GridHandle(d, key[2], key[3])
+        h = GridHandle(d, key[2], key[3], device=dev)
         _grid_cache[key] = h
     return h
 

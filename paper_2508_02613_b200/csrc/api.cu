@@ -247,8 +247,10 @@ void run_iteration_graph(jfftb_grid* g, int kind, jfftb_op* op, jfftb_jacobi* ja
   constexpr int kIterKey = jfftb_grid::kIterKey;
   const void* key[kIterKey] = {op, op->rho, jac, jac ? jac->inv_sqrt : nullptr, gpc->blocks,
                                gterm->blocks, B.x, B.st, B.hist, g->stream};
-  bool hit = g->iter_graph != nullptr && g->iter_kind == kind &&
-             g->iter_lame[0] == op->lambda0 && g->iter_lame[1] == op->mu0;
+  const double lame[6] = {op->lambda0, op->mu0, gpc->lambda_ref, gpc->mu_ref,
+                          gterm->lambda_ref, gterm->mu_ref};
+  bool hit = g->iter_graph != nullptr && g->iter_kind == kind;
+  for (int i = 0; hit && i < 6; ++i) hit = g->iter_lame[i] == lame[i];
   for (int i = 0; hit && i < kIterKey; ++i) hit = g->iter_key[i] == key[i];
   if (!hit) {
     drop_iteration_graph(g);
@@ -279,8 +281,7 @@ void run_iteration_graph(jfftb_grid* g, int kind, jfftb_op* op, jfftb_jacobi* ja
     JF_CUDA(e);
     for (int i = 0; i < kIterKey; ++i) g->iter_key[i] = key[i];
     g->iter_kind = kind;
-    g->iter_lame[0] = op->lambda0;
-    g->iter_lame[1] = op->mu0;
+    for (int i = 0; i < 6; ++i) g->iter_lame[i] = lame[i];
   }
   JF_CUDA(cudaGraphLaunch(g->iter_graph, g->stream));
   count_launch(g->iter_launches);
@@ -484,6 +485,7 @@ void op_free(jfftb_op* op) {
   {
     DeviceGuard dg(g->device);
     cudaStreamSynchronize(g->stream);
+    drop_iteration_graph(g);  // it bakes in op->rho
     cudaFree(op->rho);
   }
   delete op;
@@ -789,6 +791,7 @@ int jfftb_green_destroy(jfftb_green* green) {
     {
       DeviceGuard dg(g->device);
       cudaStreamSynchronize(g->stream);
+      drop_iteration_graph(g);  // it bakes in the Green planes
       cudaFree(green->blocks);
     }
     delete green;
@@ -898,6 +901,7 @@ int jfftb_jacobi_destroy(jfftb_jacobi* jac) {
     {
       DeviceGuard dg(op->grid->device);
       cudaStreamSynchronize(op->grid->stream);
+      drop_iteration_graph(op->grid);  // it bakes in D^-1/2
       cudaFree(jac->inv_sqrt);
     }
     delete jac;
@@ -958,7 +962,7 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     DeviceGuard dg(g->device);
     const Geom& geo = g->geo;
     cudaStream_t s = g->stream;
-    ensure_plans(g);
+    if (!g->fused) ensure_plans(g);  // the fused passes need no cuFFT plans
     const int64_t n = geo.d * geo.N;
     require(rhs != nullptr, "null right-hand side");
     require(where == JFFTB_HOST || where == JFFTB_DEVICE, "where must be HOST or DEVICE");

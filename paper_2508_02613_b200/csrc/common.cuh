@@ -53,6 +53,23 @@ inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(JFFTB_EINVAL, msg);
 }
 
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & 63;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device context:
+// `done` (one static per kernel instance) keeps one bit per device id
+template <class K>
+void set_smem_once(K kernel, size_t bytes, std::atomic<uint64_t>& done) {
+  const uint64_t bit = 1ull << current_device();
+  if (done.load() & bit) return;
+  if (bytes > 48 * 1024)
+    JF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done.fetch_or(bit);
+}
+
 // ---------------------------------------------------------------------------
 // geometry passed by value to kernels
 // ---------------------------------------------------------------------------
@@ -95,7 +112,8 @@ struct jfftb_grid {
   static constexpr int kIterKey = 10;
   cudaGraphExec_t iter_graph = nullptr;
   const void* iter_key[kIterKey] = {};
-  double iter_lame[2] = {0.0, 0.0};
+  // constants baked into the kernels' arguments: op Lame, Green (pc, term) Lame
+  double iter_lame[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int iter_kind = -1;
   int iter_launches = 0;
   size_t fft_work_bytes = 0;

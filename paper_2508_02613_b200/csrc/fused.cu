@@ -739,12 +739,6 @@ __global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
   }
 }
 
-template <class K>
-void set_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024)
-    JF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
-
 FGeom fgeom(const Geom& g) {
   FGeom f{};
   f.d = g.d;
@@ -766,8 +760,8 @@ void launchA_MT(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, c
   constexpr int NT = passA_nt(M, F, TW);
   const size_t smem = sizeof(double2) * F * TW * M;
   auto k = passA<M, F, MODE, TW>;
-  static bool attr = false;
-  if (!attr) { set_smem(k, smem); attr = true; }
+  static std::atomic<uint64_t> attr{0};
+  set_smem_once(k, smem, attr);
   dim3 grid((unsigned)(g.PS / TW), g.d);
   k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
   JF_LAUNCHED();
@@ -797,8 +791,8 @@ void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, co
       constexpr int NT = passA3_nt<M>();
       const size_t smem = sizeof(double2) * 2 * TW * M;
       auto k = passA3_fused_last() ? passA3<M, MODE, true> : passA3<M, MODE, false>;
-      static bool attr = false;
-      if (!attr) { set_smem(k, smem); attr = true; }
+      static std::atomic<uint64_t> attr{0};
+      set_smem_once(k, smem, attr);
       dim3 grid((unsigned)(g.PS / TW), g.d);
       k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
       JF_LAUNCHED();
@@ -814,8 +808,8 @@ void launchB_L(const FGeom& g, cudaStream_t s, const PcgState* st, double2* spec
   constexpr int NT = nt_for(TW * L / 8);
   const size_t smem = sizeof(double2) * TW * L;
   auto k = passB<L, INV, PRED>;
-  static bool attr = false;
-  if (!attr) { set_smem(k, smem); attr = true; }
+  static std::atomic<uint64_t> attr{0};
+  set_smem_once(k, smem, attr);
   dim3 grid((unsigned)(g.nlast / TW), g.K0, ncomp);
   k<<<grid, NT, smem, s>>>(g, st, spec, comp0, g.nlast, tw);
   JF_LAUNCHED();
@@ -827,11 +821,14 @@ int launchC_V(const FGeom& g, cudaStream_t s, const PcgState* st, const double* 
   constexpr int NT = passC_nt(D, L, F);
   const size_t smem = sizeof(double) * passC_bufd(D, L, F, GS);
   auto k = passC<D, L, F, MODE, GS, IP>;
-  static int per_sm = -1;  // per instantiation
-  if (per_sm < 0) {
-    set_smem(k, smem);
-    JF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, smem));
+  static std::atomic<uint64_t> attr{0};
+  static int per_sm_dev[64];  // per instantiation and device
+  const int dev = current_device();
+  if (!(attr.load() & (1ull << dev))) {
+    set_smem_once(k, smem, attr);
+    JF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_dev[dev], k, NT, smem));
   }
+  const int per_sm = per_sm_dev[dev];
   const int64_t rows = g.CS / L;
   const int blocks = (int)std::min<int64_t>(rows, (int64_t)std::max(per_sm, 1) * 148 * 4);
   k<<<blocks, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, ga);
@@ -870,8 +867,8 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
   constexpr int NT = passI_nt(M);
   const size_t smem = sizeof(double2) * TW * (M + 1);
   auto k = passI<M, MODE>;
-  static bool attr = false;
-  if (!attr) { set_smem(k, smem); attr = true; }
+  static std::atomic<uint64_t> attr{0};
+  set_smem_once(k, smem, attr);
   dim3 grid((unsigned)(g.PS / TW), g.d);
   k<<<grid, NT, smem, s>>>(g, st, zspec, dinv, p, x, out, tw);
   JF_LAUNCHED();

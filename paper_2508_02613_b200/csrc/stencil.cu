@@ -415,12 +415,8 @@ void launch_mode(const Geom& g, cudaStream_t s, const StencilLaunch& L, const do
                  const double* rho, double lam, double mu, const EbarT& E, double* out,
                  double* partials) {
   if (g.d == 3) {
-    static bool attr = false;  // per template instance
-    if (!attr) {
-      JF_CUDA(cudaFuncSetAttribute(stencil3d<MODE, SCALE>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S3_BYTES));
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};  // per template instance and device
+    set_smem_once(stencil3d<MODE, SCALE>, S3_BYTES, attr);
     stencil3d<MODE, SCALE><<<L.grid, L.block, S3_BYTES, s>>>(g, u, rho, lam, mu, E, out,
                                                              partials, L.chunk);
   }

@@ -127,7 +127,8 @@ def load_field_device(basepath, device="cuda"):
     raw = torch.from_numpy(_read_raw(base, header)).to(device)
     planes = _nplanes(kind, d)
     out = torch.empty_like(raw)
-    h = N.grid_handle(d, (n,) * d, grid.lengths)
+    # the reorder runs on the tensor's own device (not JFFTB_DEVICE)
+    h = N.grid_handle(d, (n,) * d, grid.lengths, device=out.device.index)
     torch.cuda.current_stream(out.device).synchronize()
     N.check(N.load().jfftb_field_layout(h.ptr, C.c_void_p(raw.data_ptr()),
                                         C.c_void_p(out.data_ptr()), planes, 1, N.DEVICE))
@@ -147,7 +148,7 @@ def save_field_device(basepath, kind: str, grid, tensor) -> None:
     if t.dtype != torch.float64 or t.numel() != planes * grid.n ** d:
         raise ValueError("tensor does not hold a float64 field of that kind and grid")
     out = torch.empty_like(t)
-    h = N.grid_handle(d, (grid.n,) * d, grid.lengths)
+    h = N.grid_handle(d, (grid.n,) * d, grid.lengths, device=t.device.index)
     torch.cuda.current_stream(t.device).synchronize()
     N.check(N.load().jfftb_field_layout(h.ptr, C.c_void_p(t.data_ptr()),
                                         C.c_void_p(out.data_ptr()), planes, 0, N.DEVICE))

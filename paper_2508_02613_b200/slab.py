@@ -98,8 +98,11 @@ class SlabComm:
         last = ext[:, L0].contiguous()
         from_prev = torch.empty_like(first)
         from_next = torch.empty_like(first)
-        ops = [dist.P2POp(dist.isend, first, prev, self.group, tag=1),
-               dist.P2POp(dist.isend, last, nxt, self.group, tag=2),
+        # NCCL ignores tags and matches the sends and receives between one
+        # pair of ranks in posting order; at world 2 (prev == nxt) the order
+        # below pairs last -> from_prev and first -> from_next on both ranks
+        ops = [dist.P2POp(dist.isend, last, nxt, self.group, tag=2),
+               dist.P2POp(dist.isend, first, prev, self.group, tag=1),
                dist.P2POp(dist.irecv, from_prev, prev, self.group, tag=2),
                dist.P2POp(dist.irecv, from_next, nxt, self.group, tag=1)]
         self._p2p(ops)
