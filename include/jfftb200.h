@@ -201,6 +201,46 @@ int jfftb_profile_start(jfftb_grid* g);
  * (iterations that ran past convergence are not counted); stop != 0 disables */
 int jfftb_profile_read(jfftb_grid* g, double* stage_ms, int64_t* iterations, int stop);
 
+/* ---- distributed 3-D solves (replaces the loop of
+ * solver.py:113-136 and the FFT solve of preconditioners.py:83-94 on
+ * slab-decomposed grids) --------------------------------------------------
+ * Real space is split into P slabs of L1 = n1 / P rows along axis 1 (rank r
+ * owns rows [r L1, (r+1) L1)); spectra into P slabs of axis-0 frequency rows.
+ * A communicator is either NCCL (one process per GPU; rank 0 makes the
+ * 128-byte unique id with jfftb_comm_unique_id and the caller broadcasts it)
+ * or a loopback that emulates all P ranks in this process on one device
+ * (ranks run one after the other; transfers are device copies).  Every
+ * per-rank array argument below holds the LOCAL ranks' slabs back to back:
+ * one slab (n0 x L1 x n2 scalars, 3 x n0 x L1 x n2 vectors) for NCCL, P for
+ * the loopback. */
+typedef struct jfftb_comm jfftb_comm;
+typedef struct jfftb_dist jfftb_dist;
+int jfftb_comm_unique_id(char* id128);
+int jfftb_comm_create_nccl(const char* id128, int rank, int world, int device, jfftb_comm** out);
+int jfftb_comm_create_local(int world, int device, jfftb_comm** out);
+int jfftb_comm_destroy(jfftb_comm* comm);
+/* make_operator + assemble_green + build_preconditioner on the slabs:
+ * power-of-two n (16..2048), n1 / P >= 16, (n0 / 2) % P == 0; kind is
+ * JFFTB_PC_GREEN or JFFTB_PC_GREEN_JACOBI; the Green operator (reference
+ * material lambda_ref, mu_ref) serves the preconditioner and the
+ * termination functional.  rho: the local density slabs (`where`). */
+int jfftb_dist_create(jfftb_comm* comm, const int64_t* n, const double* lengths, const double* rho,
+                      int where, double lambda0, double mu0, double lambda_ref, double mu_ref,
+                      int kind, jfftb_dist** out);
+int jfftb_dist_destroy(jfftb_dist* dist);
+/* assemble_rhs (operators.py:61) into the local vector slabs */
+int jfftb_dist_assemble_rhs(jfftb_dist* dist, const double* eps_bar, double* out, int where);
+/* JacobiDiagonal.inv_sqrt of the local slabs (green-jacobi) */
+int jfftb_dist_jacobi_export(jfftb_dist* dist, double* out, int where);
+/* pcg (solver.py:64-140): rhs / x_out local vector slabs; history_out (host,
+ * max_iter + 1) identical on every rank; same status codes as jfftb_pcg */
+int jfftb_dist_pcg(jfftb_dist* dist, const double* rhs, int where, double eta, int max_iter,
+                   double* x_out, double* history_out, int* iterations, int* terminated,
+                   double* wall_s);
+/* info8: world, L1, local ranks, first local rank, its k0lo, its k0 count,
+ * nodes per slab, loopback flag */
+int jfftb_dist_info(jfftb_dist* dist, int64_t* info8);
+
 /* ---- diagnostics (tests only) ------------------------------------------ */
 /* Run the fused Green(-Jacobi) application up to pass `upto` (1 axis-0 R2C,
  * 2 axis-1 FFT, 3 last-axis FFT + block solve + iFFT, 4 axis-1 iFFT,

@@ -18,7 +18,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libjfftb200.so")
-SOURCES = ["api.cu", "stencil.cu", "blas.cu", "spectral.cu", "pcg.cu", "fused.cu", "hostio.cu", "generators.cu", "loadcases.cu"]
+SOURCES = ["api.cu", "stencil.cu", "blas.cu", "spectral.cu", "pcg.cu", "fused.cu", "hostio.cu", "generators.cu", "loadcases.cu", "dist.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -310,9 +310,11 @@ enum StencilMode { ST_K = 0, ST_RHS = 1, ST_RES = 2 };
 // out = K u (ST_K), -B^T W rho C E (ST_RHS), -B^T W sigma(E + B u) (ST_RES).
 // rho == nullptr means rho = 1.  curv_partials (ST_K only, may be null):
 // per-block <u, out> partials; returns number of blocks written.
+// ext = 1 (3-D): u and rho are halo-extended slabs with n[1] + 2 rows along
+// axis 1 (row i of out reads input rows i .. i + 2); no wrap along axis 1
 int launch_stencil(const Geom& g, cudaStream_t s, int mode, const double* u,
                    const double* rho, double lam, double mu, const double* ebar_mandel,
-                   double* out, double* curv_partials);
+                   double* out, double* curv_partials, int ext = 0);
 int stencil_blocks(const Geom& g);
 
 void launch_total_strain(const Geom& g, cudaStream_t s, const double* u,
@@ -389,8 +391,10 @@ void launch_green_apply(const Geom& g, cudaStream_t s, const double* blocks,
 // resp: d x d x prod(m) impulse responses on the small grid m (packed m0|m1<<8|m2<<16)
 // layout 0: numpy rfftn order (last axis halved), nfreq = Nh; layout 1:
 // fused.cu order (axis 0 halved), nfreq = fused_spec_elems
+// k0_off (layout 1): first axis-0 frequency of a k0-slab (distributed solves)
 void launch_green_setup(const Geom& g, cudaStream_t s, const double* resp, int m,
-                        double* blocks, int layout, int64_t nfreq, bool dif_last = false);
+                        double* blocks, int layout, int64_t nfreq, bool dif_last = false,
+                        int k0_off = 0);
 
 // PCG (pcg.cu)
 struct PcgBuffers {
@@ -432,6 +436,27 @@ void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st
                    const double2* zspec, const double* dinv, double* p, double* x,
                    const double2* tw);
 int64_t fused_component_stride(const Geom& geo);
+// distributed solves (dist.cu): one rank's k0-slab of the spectral passes
+struct SpecSlab {
+  int k0lo, kcnt;  // axis-0 frequency rows [k0lo, k0lo + kcnt)
+  int L1;          // axis-1 rows per source rank (segments of n1 / L1 ranks)
+  int nf;          // fields held (2d green-jacobi, d green)
+};
+void fused_stage_B_slab(const Geom& geo, const SpecSlab& sl, cudaStream_t s, bool inv,
+                        const PcgState* st, double2* recv, int comp0, int ncomp,
+                        const double2* tw);
+int fused_stage_C_slab(const Geom& geo, const SpecSlab& sl, cudaStream_t s, int F,
+                       const PcgState* st, const double* green, double2* recv, double* partials,
+                       const double2* tw);
+void fused_stage_I_ext(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
+                       const double2* zspec, const double* dinv, double* p_ext, double* x,
+                       const double2* tw);
+// PCG scalar kernels (pcg.cu) over `count` partials: alpha = rz / curvature,
+// and the termination test / beta (solver.py:115-135)
+// (partial j of block b at partials[b * stride + j])
+void launch_alpha(cudaStream_t s, PcgState* st, const double* partials, int count, int stride);
+void launch_finalize(int kind, bool init, cudaStream_t s, PcgState* st, const double* spart,
+                     int scount, int sstride, double* hist);
 void fused_debug_apply(const Geom& geo, cudaStream_t s, const jfftb_green* green,
                        const double* dinv, const double* r, double* out, double2* spec,
                        const double2* tw, int upto);

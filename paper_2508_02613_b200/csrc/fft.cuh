@@ -186,12 +186,18 @@ __host__ __device__ constexpr int padded_len(int L) {
 // contiguous at gin + q * gqs) instead of buf; GOUT: the last stage writes
 // its outputs to gout + q * gqs (no trailing barrier -- buf is only read).
 template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, int S, int NS, bool WARP = false,
-          bool GIN = false, bool GOUT = false>
+          bool GIN = false, bool GOUT = false, bool SEG = false>
 __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
                                               const double2* __restrict__ tw,
                                               const double2* gin = nullptr,
                                               double2* gout = nullptr, int64_t gqs = 0,
-                                              int64_t gks = 1) {
+                                              int64_t gks = 1, int gsh = 0, int64_t gss = 0) {
+  // global element k of a sequence: k gks, or with SEG the segmented
+  // (k >> gsh) gss + (k & (2^gsh - 1)) gks
+  auto gix = [&](int k) -> int64_t {
+    if constexpr (SEG) return (int64_t)(k >> gsh) * gss + (int64_t)(k & ((1 << gsh) - 1)) * gks;
+    else return (int64_t)k * gks;
+  };
   if constexpr (S < fft_nstages(L)) {
     constexpr bool FROM_G = GIN && S == 0;
     constexpr bool TO_G = GOUT && S + 1 == fft_nstages(L);
@@ -224,7 +230,7 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
         if constexpr (FROM_G) {
           const double2* src = gin + qq[m] * gqs;
 #pragma unroll
-          for (int t = 0; t < R; ++t) v[m][t] = src[(jj[m] + t * NB) * gks];
+          for (int t = 0; t < R; ++t) v[m][t] = src[gix(jj[m] + t * NB)];
         } else {
           const double2* src = buf + qq[m] * qs;
 #pragma unroll
@@ -253,7 +259,7 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
         if constexpr (TO_G) {
           double2* dst = gout + qq[m] * gqs;
 #pragma unroll
-          for (int t = 0; t < R; ++t) dst[(o + t * NS) * gks] = v[m][t];
+          for (int t = 0; t < R; ++t) dst[gix(o + t * NS)] = v[m][t];
         } else {
           double2* dst = buf + qq[m] * qs;
 #pragma unroll
@@ -264,8 +270,8 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
     if constexpr (!TO_G) {
       if (WARP) __syncwarp(); else __syncthreads();
     }
-    cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, S + 1, NS * R, WARP, GIN, GOUT>(buf, ks, qs, tw,
-                                                                             gin, gout, gqs, gks);
+    cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, S + 1, NS * R, WARP, GIN, GOUT, SEG>(
+        buf, ks, qs, tw, gin, gout, gqs, gks, gsh, gss);
   }
 }
 
@@ -280,12 +286,14 @@ __device__ __forceinline__ void cta_fft(double2* buf, int ks, int qs,
 // reads the first stage's inputs from gin + q * gqs + k * gks (no prior smem
 // staging; the caller barriers before, as buf is written by the first
 // stage), GOUT writes the last stage's outputs to gout + q * gqs + k * gks.
-template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, bool GIN, bool GOUT>
+template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, bool GIN, bool GOUT,
+          bool SEG = false>
 __device__ __forceinline__ void cta_fft_io(double2* buf, int ks, int qs,
                                            const double2* __restrict__ tw, const double2* gin,
-                                           double2* gout, int64_t gqs, int64_t gks) {
-  cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, 0, 1, false, GIN, GOUT>(buf, ks, qs, tw, gin, gout,
-                                                                      gqs, gks);
+                                           double2* gout, int64_t gqs, int64_t gks, int gsh = 0,
+                                           int64_t gss = 0) {
+  cta_fft_stage<L, NSEQ, NT, INV, QFAST, PAD, 0, 1, false, GIN, GOUT, SEG>(
+      buf, ks, qs, tw, gin, gout, gqs, gks, gsh, gss);
 }
 
 // ---------------------------------------------------------------------------

@@ -56,11 +56,25 @@ enum FMode { FM_APPLY = FUSED_APPLY, FM_INIT = FUSED_INIT, FM_ITER = FUSED_ITER,
 
 struct FGeom {
   int d, n0, nlast;
-  int M0, K0;      // n0 / 2, n0 / 2 + 1
+  int M0, K0;      // n0 / 2, n0 / 2 + 1 (spectral passes B, C: the k0 rows held here)
   int64_t PS;      // elements per axis-0 plane (= N / n0)
   int64_t CS;      // complex elements per spectral component (= K0 * PS)
   int64_t N;
   int n1;          // d = 3: axis-1 extent
+  // spectral-pass addressing (B, C).  Frequency row (k, k1) of field f sits
+  // at f FS + (k1 >> sh) SS + k KS + (k1 & (2^sh - 1)) nlast: one segment per
+  // source rank of a distributed solve (dist.cu), a single segment (SS = 0,
+  // KS = PS, FS = CS) on one GPU.  k0lo: global index of the first k0 row.
+  int64_t FS, KS, SS;
+  int sh, rsh;     // segment shift; log2(rows per k0 row = PS / nlast)
+  int k0lo;
+  // pass I: the direction p may live in a halo-extended slab (dist.cu)
+  int64_t pN, pPS, poff;
+  __device__ __forceinline__ int64_t row_off(int64_t row) const {
+    const int64_t k = row >> rsh;
+    const int k1 = (int)(row & ((1 << rsh) - 1));
+    return (int64_t)(k1 >> sh) * SS + k * KS + (int64_t)(k1 & ((1 << sh) - 1)) * nlast;
+  }
 };
 
 constexpr int tw_a(int M) { return M >= 1024 ? 4 : (M >= 512 ? 8 : 16); }
@@ -309,7 +323,7 @@ __global__ void __launch_bounds__(passA3_nt<M>(), 1)
 // pass B: complex FFT along axis 1 (d = 3), in place, components
 // [comp0, comp0 + gridDim.z)
 // ---------------------------------------------------------------------------
-template <int L, bool INV, bool PRED>
+template <int L, bool INV, bool PRED, bool SEG>
 __global__ void __launch_bounds__(nt_for(tw_b(L) * L / 8))
     passB(FGeom g, const PcgState* __restrict__ st, double2* __restrict__ spec, int comp0,
           int nlast, const double2* __restrict__ tw) {
@@ -320,11 +334,13 @@ __global__ void __launch_bounds__(nt_for(tw_b(L) * L / 8))
   const int c = comp0 + blockIdx.z;
   const int k0 = blockIdx.y;
   const int64_t col0 = (int64_t)blockIdx.x * TW;
-  double2* base = spec + c * g.CS + (int64_t)k0 * g.PS + col0;
+  double2* base = spec + c * g.FS + (int64_t)k0 * g.KS + col0;
   // column col of the tile is sequence col: element i at base + i nlast + col
   // (TW columns = 128-byte row segments), read by the first stage and written
-  // by the last straight from/to global memory
-  cta_fft_io<L, TW, NT, INV, true, 0, true, true>(sbuf, TW, 1, tw, base, base, 1, nlast);
+  // by the last straight from/to global memory; SEG: element i at
+  // base + (i >> sh) SS + (i & (2^sh - 1)) nlast (per-rank segments)
+  cta_fft_io<L, TW, NT, INV, true, 0, true, true, SEG>(sbuf, TW, 1, tw, base, base, 1, nlast,
+                                                       g.sh, g.SS);
 }
 
 // ---------------------------------------------------------------------------
@@ -546,20 +562,22 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
   int64_t row = blockIdx.x;
   if (row < rows) prefetch_green(row);
   for (; row < rows; row += gridDim.x) {
-    const int64_t rbase = row * L;
-    const int k0 = (int)row / (int)(g.PS / L);
+    const int64_t rbase = row * L;        // Green planes: rows back to back
+    const int64_t sbase = g.row_off(row);  // spectra: (segmented) row address
+    const int k0 = g.k0lo + (int)(row >> g.rsh);
     const double w = (k0 == 0 || 2 * k0 == g.n0) ? 1.0 : 2.0;
     // forward: global rows -> (stage 1) -> shared; barrier-separated from the
     // previous row-set's last shared-memory reads by the loop-end barrier
     if constexpr (IP)
-      cta_fft_dif<L, NQ, NT, CPAD, true>(sbuf, RL, tw, spec + rbase, g.CS);
+      cta_fft_dif<L, NQ, NT, CPAD, true>(sbuf, RL, tw, spec + sbase, g.FS);
     else
-      cta_fft_io<L, NQ, NT, false, false, CPAD, true, false>(sbuf, 1, RL, tw, spec + rbase,
-                                                             nullptr, g.CS, 1);
+      cta_fft_io<L, NQ, NT, false, false, CPAD, true, false>(sbuf, 1, RL, tw, spec + sbase,
+                                                             nullptr, g.FS, 1);
 #ifndef JF_NO_PREFETCH
     // the next row-set's rows into L2 while this one is solved and inverted
     if (threadIdx.x < NQ && row + gridDim.x < rows)
-      bulk_prefetch_l2(spec + threadIdx.x * g.CS + (row + gridDim.x) * L, L * sizeof(double2));
+      bulk_prefetch_l2(spec + threadIdx.x * g.FS + g.row_off(row + gridDim.x),
+                       L * sizeof(double2));
 #endif
     if (GS == 1) mbar_wait(&gbar, gphase);  // this row-set's Green planes
     gphase ^= 1;
@@ -567,7 +585,7 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     GRow grow;
     bool dcrow = false;  // the row holding the zero frequency
     if constexpr (GS == 2) {
-      const int k1 = (int)(row % (g.PS / L));
+      const int k1 = (int)(row & ((1 << g.rsh) - 1));
       grow = green_row(ga, cconj(__ldg(tw + ((k0 * (kTwN / g.n0)) & (kTwN - 1)))),
                        cconj(__ldg(tw + ((k1 * (kTwN / g.n1)) & (kTwN - 1)))));
       dcrow = k0 == 0 && k1 == 0;
@@ -624,11 +642,11 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     if (row + gridDim.x < rows) prefetch_green(row + gridDim.x);
     if (MODE != FM_QUAD) {
       if constexpr (IP)
-        cta_fft_dit_inv<L, D, NT, CPAD, true>(sbuf + ZQ * RL, RL, tw, spec + ZQ * g.CS + rbase,
-                                              g.CS);
+        cta_fft_dit_inv<L, D, NT, CPAD, true>(sbuf + ZQ * RL, RL, tw, spec + ZQ * g.FS + sbase,
+                                              g.FS);
       else
         cta_fft_io<L, D, NT, true, false, CPAD, false, true>(sbuf + ZQ * RL, 1, RL, tw, nullptr,
-                                                             spec + ZQ * g.CS + rbase, g.CS, 1);
+                                                             spec + ZQ * g.FS + sbase, g.FS, 1);
     }
     __syncthreads();
   }
@@ -683,6 +701,7 @@ __global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
   constexpr int RAWN = 2 * M * TW;  // real elements of the tile
   const bool use_d = dinv != nullptr;
   const int64_t cbase = c * g.N + col0;
+  const int64_t pbase = c * g.pN + g.poff + col0;
   cpa_wait<0>();
   __syncthreads();
   // Z'[k] = (X[k] + conj X[M-k]) + i e^{+2 pi i k / n0} (X[k] - conj X[M-k]),
@@ -717,23 +736,25 @@ __global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
     for (int j = 0; j < CH; ++j) {
       const int e = threadIdx.x + (j0 + j) * NT;
       const int64_t idx = cbase + (int64_t)(e / TW) * g.PS + (e % TW);
+      const int64_t pix = pbase + (int64_t)(e / TW) * g.pPS + (e % TW);
       if (use_d) dv[j] = __ldg(dinv + idx);
-      if (MODE == FM_ITER) { pv[j] = p[idx]; xv[j] = x[idx]; }
+      if (MODE == FM_ITER) { pv[j] = p[pix]; xv[j] = x[idx]; }
     }
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
       const int e = threadIdx.x + (j0 + j) * NT;
       const int i0 = e / TW, col = e % TW;
       const int64_t idx = cbase + (int64_t)i0 * g.PS + col;
+      const int64_t pix = pbase + (int64_t)i0 * g.pPS + col;
       double zz = zr[((i0 >> 1) * TW + col) * 2 + (i0 & 1)];
       if (use_d) zz = dv[j] * zz;
       if (MODE == FM_APPLY) {
         out[idx] = zz;
       } else if (MODE == FM_INIT) {
-        p[idx] = zz;
+        p[pix] = zz;
       } else {
         x[idx] = xv[j] + alpha * pv[j];
-        if (!done) p[idx] = beta * pv[j] + zz;
+        if (!done) p[pix] = beta * pv[j] + zz;
       }
     }
   }
@@ -750,6 +771,15 @@ FGeom fgeom(const Geom& g) {
   f.PS = g.N / g.n[0];
   f.CS = (int64_t)f.K0 * f.PS;
   f.n1 = g.d == 3 ? g.n[1] : 1;
+  f.FS = f.CS;
+  f.KS = f.PS;
+  f.SS = 0;
+  f.rsh = ilog2c((int)(f.PS / f.nlast));
+  f.sh = f.rsh;
+  f.k0lo = 0;
+  f.pN = f.N;
+  f.pPS = f.PS;
+  f.poff = 0;
   return f;
 }
 
@@ -807,7 +837,7 @@ void launchB_L(const FGeom& g, cudaStream_t s, const PcgState* st, double2* spec
   constexpr int TW = tw_b(L);
   constexpr int NT = nt_for(TW * L / 8);
   const size_t smem = sizeof(double2) * TW * L;
-  auto k = passB<L, INV, PRED>;
+  auto k = g.SS != 0 ? passB<L, INV, PRED, true> : passB<L, INV, PRED, false>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
   dim3 grid((unsigned)(g.nlast / TW), g.K0, ncomp);
@@ -1045,5 +1075,44 @@ void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st
   launchI(fgeom(geo), s, mode, st, zspec, dinv, p, x, nullptr, tw);
 }
 int64_t fused_component_stride(const Geom& geo) { return fgeom(geo).CS; }
+
+// ---- distributed solves (dist.cu) ------------------------------------------
+// The spectral passes of one rank's k0-slab: frequency rows k0 in
+// [k0lo, k0lo + kcnt) of the global grid `geo`, received from P = n1 / L1
+// ranks into [src][field (nf)][k0][i1 local (L1)][i2] (one segment per source
+// rank, field stride kcnt L1 n2, segment stride nf times that).
+FGeom fgeom_slab(const Geom& geo, const SpecSlab& sl) {
+  FGeom g = fgeom(geo);
+  g.K0 = sl.kcnt;
+  g.k0lo = sl.k0lo;
+  g.CS = (int64_t)sl.kcnt * g.PS;  // elements per field (rows kcnt x n1)
+  g.KS = (int64_t)sl.L1 * g.nlast;
+  g.FS = (int64_t)sl.kcnt * g.KS;
+  g.SS = (int64_t)sl.nf * g.FS;
+  g.sh = ilog2c(sl.L1);
+  return g;
+}
+void fused_stage_B_slab(const Geom& geo, const SpecSlab& sl, cudaStream_t s, bool inv,
+                        const PcgState* st, double2* recv, int comp0, int ncomp,
+                        const double2* tw) {
+  launchB(fgeom_slab(geo, sl), s, inv, true, st, recv, comp0, ncomp, tw);
+}
+int fused_stage_C_slab(const Geom& geo, const SpecSlab& sl, cudaStream_t s, int F,
+                       const PcgState* st, const double* green, double2* recv, double* partials,
+                       const double2* tw) {
+  const FGeom g = fgeom_slab(geo, sl);
+  return launchC(g, s, F, FM_ITER, st, green, green, recv, partials, tw, GreenAna{}, false);
+}
+// pass I of a rank whose direction p lives in a halo-extended slab of
+// n1 + 2 rows along axis 1 (geo: the rank's local real-space slab)
+void fused_stage_I_ext(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
+                       const double2* zspec, const double* dinv, double* p_ext, double* x,
+                       const double2* tw) {
+  FGeom g = fgeom(geo);
+  g.pPS = (int64_t)(geo.n[1] + 2) * geo.n[2];
+  g.pN = (int64_t)geo.n[0] * g.pPS;
+  g.poff = geo.n[2];  // row 0 of the extended slab is the lower halo
+  launchI(g, s, mode, st, zspec, dinv, p_ext, x, nullptr, tw);
+}
 
 }  // namespace jfftb

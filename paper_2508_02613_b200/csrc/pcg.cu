@@ -42,13 +42,14 @@ __device__ double sum_strided(const double* p, int count, int stride, int j, dou
   return s;  // valid in thread 0
 }
 
-__global__ void alpha_kernel(PcgState* st, const double* __restrict__ partials, int count) {
+__global__ void alpha_kernel(PcgState* st, const double* __restrict__ partials, int count,
+                             int stride) {
   __shared__ double red[32];
   if (st->done) {
     if (threadIdx.x == 0) st->xupd = 0;
     return;
   }
-  const double curv = sum_strided(partials, count, 1, 0, red);
+  const double curv = sum_strided(partials, count, stride, 0, red);
   if (threadIdx.x == 0) {
     st->curv = curv;
     st->xupd = 0;
@@ -101,12 +102,12 @@ __global__ void __launch_bounds__(256)
 // termination test + beta (solver.py:122-135); INIT = the k = 0 check (99-110)
 template <int KIND, bool INIT>
 __global__ void finalize_kernel(PcgState* st, const double* __restrict__ spart, int scount,
-                                const double* __restrict__ upart, int ucount,
+                                int sstride, const double* __restrict__ upart, int ucount,
                                 double* __restrict__ hist) {
   __shared__ double red[32];
   if (st->done) return;
-  const double q0 = sum_strided(spart, scount, 2, 0, red);
-  const double q1 = sum_strided(spart, scount, 2, 1, red);
+  const double q0 = sum_strided(spart, scount, sstride, 0, red);
+  const double q1 = sum_strided(spart, scount, sstride, 1, red);
   double u0 = 0.0;
   if (KIND == JFFTB_PC_JACOBI || KIND == JFFTB_PC_NONE) u0 = sum_strided(upart, ucount, 1, 0, red);
   if (threadIdx.x != 0) return;
@@ -188,8 +189,8 @@ static void pcg_precond_phase(jfftb_grid* g, jfftb_jacobi* jac, jfftb_green* gpc
   launch_pcg_spectral(geo, s, mode, (mode == 2 ? gterm : gpc)->blocks, gterm->blocks, B.spec,
                       B.st, B.spart);
   if (!INIT) prof_mark(g);
-  finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, kRedBlocks, B.upart, kRedBlocks,
-                                                 B.hist);
+  finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, kRedBlocks, 2, B.upart,
+                                                 kRedBlocks, B.hist);
   JF_LAUNCHED();
   if (!INIT) prof_mark(g);
   const double* zsrc = r;
@@ -247,8 +248,8 @@ static void pcg_precond_phase_fused(jfftb_grid* g, jfftb_jacobi* jac, jfftb_gree
     scount = fused_stage_C(geo, s, 1, true, B.st, gterm, gterm, B.spec, B.spart, tw);
   }
   if (!INIT) prof_mark(g);
-  finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, scount, B.upart, kRedBlocks,
-                                                 B.hist);
+  finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, scount, 2, B.upart,
+                                                 kRedBlocks, B.hist);
   JF_LAUNCHED();
   if (!INIT) prof_mark(g);
   if (SPECTRAL_PC) {
@@ -277,7 +278,7 @@ static void pcg_iteration(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
   prof_mark(g);
   launch_stencil(g->geo, s, ST_K, B.p, op->rho, op->lambda0, op->mu0, nullptr, B.kp, B.kpart);
   prof_mark(g);
-  alpha_kernel<<<1, 1024, 0, s>>>(B.st, B.kpart, B.kcount);
+  alpha_kernel<<<1, 1024, 0, s>>>(B.st, B.kpart, B.kcount, 1);
   JF_LAUNCHED();
   prof_mark(g);
   if (g->fused) pcg_precond_phase_fused<KIND, false>(g, jac, gpc, gterm, B);
@@ -289,6 +290,25 @@ static void pcg_init(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc, jfftb_gr
                      const PcgBuffers& B) {
   if (op->grid->fused) pcg_precond_phase_fused<KIND, true>(op->grid, jac, gpc, gterm, B);
   else pcg_precond_phase<KIND, true>(op->grid, jac, gpc, gterm, B);
+}
+
+void launch_alpha(cudaStream_t s, PcgState* st, const double* partials, int count, int stride) {
+  alpha_kernel<<<1, 1024, 0, s>>>(st, partials, count, stride);
+  JF_LAUNCHED();
+}
+
+void launch_finalize(int kind, bool init, cudaStream_t s, PcgState* st, const double* spart,
+                     int scount, int sstride, double* hist) {
+  require(kind == JFFTB_PC_GREEN || kind == JFFTB_PC_GREEN_JACOBI,
+          "finalize: spectral kinds only");
+  if (kind == JFFTB_PC_GREEN) {
+    init ? finalize_kernel<JFFTB_PC_GREEN, true><<<1, 1024, 0, s>>>(st, spart, scount, sstride, nullptr, 0, hist)
+         : finalize_kernel<JFFTB_PC_GREEN, false><<<1, 1024, 0, s>>>(st, spart, scount, sstride, nullptr, 0, hist);
+  } else {
+    init ? finalize_kernel<JFFTB_PC_GREEN_JACOBI, true><<<1, 1024, 0, s>>>(st, spart, scount, sstride, nullptr, 0, hist)
+         : finalize_kernel<JFFTB_PC_GREEN_JACOBI, false><<<1, 1024, 0, s>>>(st, spart, scount, sstride, nullptr, 0, hist);
+  }
+  JF_LAUNCHED();
 }
 
 void pcg_dispatch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,

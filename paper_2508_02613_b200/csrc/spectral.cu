@@ -216,7 +216,7 @@ __device__ void herm_pinv(const double (&Hr)[D][D], const double (&Hi)[D][D],
 template <int D>
 __global__ void green_setup_kernel(Geom g, const double* __restrict__ resp, int m0, int m1,
                                    int m2, double* __restrict__ blocks, int layout,
-                                   bool dif_last, int64_t nfreq) {
+                                   bool dif_last, int64_t nfreq, int k0_off) {
   // resp: D impulse responses (beta) of D components on the small m-grid
   const int m[3] = {m0, m1, m2};
   int64_t msz = 1;
@@ -240,7 +240,7 @@ __global__ void green_setup_kernel(Geom g, const double* __restrict__ resp, int 
       if (D == 3) q[0] = (int)rem;
     } else {
       for (int a = D - 1; a >= 1; --a) { q[a] = (int)(rem % g.n[a]); rem /= g.n[a]; }
-      q[0] = (int)rem;
+      q[0] = (int)rem + k0_off;  // k0-slab of a distributed solve (dist.cu)
       // slot -> frequency of the in-place last-axis transform (fused pass C)
       if (dif_last) q[D - 1] = dif_freq(g.n[D - 1], q[D - 1]);
     }
@@ -327,15 +327,15 @@ void launch_green_apply(const Geom& g, cudaStream_t s, const double* blocks, con
 }
 
 void launch_green_setup(const Geom& g, cudaStream_t s, const double* resp, int m3, double* blocks,
-                        int layout, int64_t nfreq, bool dif_last) {
+                        int layout, int64_t nfreq, bool dif_last, int k0_off) {
   // m3 packs the small-grid extents as m0 | m1 << 8 | m2 << 16
   const int m0 = m3 & 0xff, m1 = (m3 >> 8) & 0xff, m2 = (m3 >> 16) & 0xff;
   if (g.d == 3)
     green_setup_kernel<3><<<spec_blocks(nfreq), 128, 0, s>>>(g, resp, m0, m1, m2, blocks, layout, dif_last,
-                                                             nfreq);
+                                                             nfreq, k0_off);
   else
     green_setup_kernel<2><<<spec_blocks(nfreq), 128, 0, s>>>(g, resp, m0, m1, m2, blocks, layout, dif_last,
-                                                             nfreq);
+                                                             nfreq, k0_off);
   JF_LAUNCHED();
 }
 

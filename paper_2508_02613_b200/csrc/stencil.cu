@@ -120,7 +120,7 @@ template <int MODE, bool SCALE>
 __global__ void __launch_bounds__(BX3* BY3, MINB3)
     stencil3d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
               double lam0, double mu0, EbarT E, double* __restrict__ out,
-              double* __restrict__ partials, int chunk) {
+              double* __restrict__ partials, int chunk, int ext) {
   constexpr bool HAS_U = MODE != VOX_RHS;
   extern __shared__ double smem[];
   double(*U)[3][BY3 + 1][BX3 + 1] = reinterpret_cast<double(*)[3][BY3 + 1][BX3 + 1]>(smem);
@@ -131,15 +131,21 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
 
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const int64_t P = (int64_t)n1 * n2;
+  // ext = 1 (distributed slabs, dist.cu): u and rho are halo-extended slabs
+  // of n1 + 2 rows along axis 1 (input row = output row + 1, no wrap along
+  // axis 1); out keeps the n1 rows
+  const int64_t Pin = ext ? P + 2 * (int64_t)n2 : P, Nin = (int64_t)n0 * Pin;
+  auto in_row = [&](int y) { return ext ? min(y + 1, n1 + 1) : wrapi(y, n1); };
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int X0 = blockIdx.x * (BX3 - 1), Y0 = blockIdx.y * (BY3 - 1);
   const int k0 = blockIdx.z * chunk;
   const int k1 = min(k0 + chunk, n0);
   const int gx = X0 - 1 + tx, gy = Y0 - 1 + ty;
-  const int c2 = wrapi(gx, n2), c1 = wrapi(gy, n1);
+  const int c2 = wrapi(gx, n2);
   const bool outp = tx >= 1 && ty >= 1 && gx < n2 && gy < n1;
-  const int c2h = wrapi(X0 - 1 + BX3, n2), c1h = wrapi(Y0 - 1 + BY3, n1);
-  const int64_t col = (int64_t)c1 * n2 + c2;
+  const int c2h = wrapi(X0 - 1 + BX3, n2), c1h = in_row(Y0 - 1 + BY3);
+  const int64_t col = (int64_t)(outp ? gy : 0) * n2 + c2;  // output column
+  const int64_t cin = (int64_t)in_row(gy) * n2 + c2;       // input column
   // halo of a plane: column x = BX3 (BY3 values) and row y = BY3 (BX3 + 1
   // values) of each component, 3 * 41 copies spread over the first threads
   constexpr int HPC = BY3 + BX3 + 1;  // halo values per component
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   if (h_on) {
     const int hc = tid / HPC, e = tid % HPC;
     const int hy_ = e < BY3 ? e : BY3, hx_ = e < BY3 ? BX3 : e - BY3;
-    h_src = (int64_t)hc * g.N + (int64_t)wrapi(Y0 - 1 + hy_, n1) * n2 + wrapi(X0 - 1 + hx_, n2);
+    h_src = (int64_t)hc * Nin + (int64_t)in_row(Y0 - 1 + hy_) * n2 + wrapi(X0 - 1 + hx_, n2);
     h_dst = (hc * (BY3 + 1) + hy_) * (BX3 + 1) + hx_;
   }
   (void)c2h;
@@ -168,13 +174,13 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   auto next_slot = [](int sl) { return sl == RING - 1 ? 0 : sl + 1; };
   auto fetch_u = [&](int kk, int s) {
     if (!HAS_U) return;
-    const double* ub = u + (int64_t)plane_of(kk) * P;
+    const double* ub = u + (int64_t)plane_of(kk) * Pin;
 #pragma unroll
-    for (int i = 0; i < 3; ++i) cp_async8(&U[s][i][ty][tx], ub + i * g.N + col);
+    for (int i = 0; i < 3; ++i) cp_async8(&U[s][i][ty][tx], ub + i * Nin + cin);
     cp_async8_if(&U[s][0][0][0] + h_dst, ub + h_src, h_on);
   };
   auto fetch_r = [&](int kk, int s) {
-    if (rho) cp_async8(&R[s][ty][tx], rho + (int64_t)plane_of(kk) * P + col);
+    if (rho) cp_async8(&R[s][ty][tx], rho + (int64_t)plane_of(kk) * Pin + cin);
   };
   auto read_corners = [&](int s, double (&q)[4][3]) {
 #pragma unroll
@@ -292,7 +298,7 @@ template <int MODE, bool SCALE>
 __global__ void __launch_bounds__(BX2)
     stencil2d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
               double lam0, double mu0, EbarT E, double* __restrict__ out,
-              double* __restrict__ partials, int chunk) {
+              double* __restrict__ partials, int chunk, int) {
   constexpr bool HAS_U = MODE != VOX_RHS;
   __shared__ double U[2][BX2 + 1];
   __shared__ double F[2][2][BX2];  // [plane][comp]
@@ -413,16 +419,16 @@ StencilLaunch stencil_config(const Geom& g) {
 template <int MODE, bool SCALE>
 void launch_mode(const Geom& g, cudaStream_t s, const StencilLaunch& L, const double* u,
                  const double* rho, double lam, double mu, const EbarT& E, double* out,
-                 double* partials) {
+                 double* partials, int ext) {
   if (g.d == 3) {
     static std::atomic<uint64_t> attr{0};  // per template instance and device
     set_smem_once(stencil3d<MODE, SCALE>, S3_BYTES, attr);
     stencil3d<MODE, SCALE><<<L.grid, L.block, S3_BYTES, s>>>(g, u, rho, lam, mu, E, out,
-                                                             partials, L.chunk);
+                                                             partials, L.chunk, ext);
   }
   else
     stencil2d<MODE, SCALE><<<L.grid, L.block, 0, s>>>(g, u, rho, lam, mu, E, out, partials,
-                                                      L.chunk);
+                                                      L.chunk, 0);
   JF_LAUNCHED();
 }
 
@@ -435,22 +441,23 @@ int stencil_blocks(const Geom& g) {
 
 int launch_stencil(const Geom& g, cudaStream_t s, int mode, const double* u, const double* rho,
                    double lam, double mu, const double* ebar_mandel, double* out,
-                   double* curv_partials) {
+                   double* curv_partials, int ext) {
+  require(!ext || g.d == 3, "halo-extended slabs are 3-D only");
   StencilLaunch L = stencil_config(g);
   const EbarT E = make_ebar(g.d, ebar_mandel);
   if (mode == ST_K) {
     if (g.iso) {
       // fold the two 1/h factors and the weight into the Lame constants
       const double sc = g.w * g.hinv[0] * g.hinv[0];
-      launch_mode<VOX_K, false>(g, s, L, u, rho, lam * sc, mu * sc, E, out, curv_partials);
+      launch_mode<VOX_K, false>(g, s, L, u, rho, lam * sc, mu * sc, E, out, curv_partials, ext);
     } else {
-      launch_mode<VOX_K, true>(g, s, L, u, rho, lam * g.w, mu * g.w, E, out, curv_partials);
+      launch_mode<VOX_K, true>(g, s, L, u, rho, lam * g.w, mu * g.w, E, out, curv_partials, ext);
     }
   } else if (mode == ST_RHS) {
     // f = -B^T W rho C E : negate through the Lame constants
-    launch_mode<VOX_RHS, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr);
+    launch_mode<VOX_RHS, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr, ext);
   } else {
-    launch_mode<VOX_RES, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr);
+    launch_mode<VOX_RES, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr, ext);
   }
   return L.grid.x * L.grid.y * L.grid.z;
 }

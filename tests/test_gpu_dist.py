@@ -1,0 +1,156 @@
+"""Distributed (slab-decomposed) PCG through the library (csrc/dist.cu).
+
+On the single test GPU the decomposition runs under the loopback
+communicator (all P ranks in one process, device copies between them, ranks
+issued one after the other) and under a one-rank NCCL communicator.  Parity
+targets: the single-GPU library solve (same kernels, different reduction
+grouping), the oracle, and bitwise equality where the arithmetic is the same
+(Jacobi diagonal, rhs, loopback P = 1 vs NCCL P = 1)."""
+
+import numpy as np
+import pytest
+
+from oracle import jfft_oracle as X
+from paper_2508_02613_b200 import dist as Dm
+from paper_2508_02613_b200 import grid as G
+from paper_2508_02613_b200 import microstructures as ms
+from paper_2508_02613_b200.material import isotropic_material
+from paper_2508_02613_b200.operators import assemble_rhs, homogenized_stress, make_operator
+from paper_2508_02613_b200.preconditioners import (assemble_green, assemble_jacobi,
+                                                   build_preconditioner)
+from paper_2508_02613_b200.solver import pcg
+
+pytestmark = pytest.mark.gpu
+
+LAM, MU = ms.lame_from_poisson()
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def density(n, seed=3):
+    return ms.random_spheres(n, count=6, rmin=n / 10, rmax=n / 5, filters=3, emin=1e-2, seed=seed)
+
+
+def single_gpu(rho, kind, eta, max_iter, eb):
+    n = rho.shape[0]
+    grid = G.make_grid(n, (1.0,) * 3)
+    mat = isotropic_material(LAM, MU, 3)
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    green = assemble_green(grid, mat)
+    rhs = assemble_rhs(op, eb)
+    rep = pcg(op, rhs, build_preconditioner(kind, op, green), green, eta=eta, max_iter=max_iter)
+    return op, rhs.values, rep
+
+
+def dist_solve(comm, rho, kind, eta, max_iter, eb):
+    n = rho.shape
+    P = comm.world
+    slabs = Dm.split(rho, P, axis=1)
+    local = np.stack(slabs) if comm.local else slabs[comm.rank]
+    D = Dm.DistSolver(comm, n, (1.0,) * 3, local, LAM, MU, kind=kind)
+    rhs = D.assemble_rhs(eb)
+    rep = D.pcg(rhs, eta=eta, max_iter=max_iter)
+    return D, rhs, rep
+
+
+def glob(local, P):
+    """(P, 3, n0, L1, n2) loopback slabs -> (3, n0, n1, n2)."""
+    return Dm.join(list(local), axis=2)
+
+
+@pytest.mark.parametrize("n,P", [(32, 1), (32, 2), (64, 4)])
+@pytest.mark.parametrize("kind", ["green-jacobi", "green"])
+def test_loopback_matches_single_gpu(n, P, kind):
+    """Same kernels, different reduction grouping: the eta = 1e-6 solves take
+    the same number of iterations (+-1); solved far below that (eta = 1e-28,
+    ~1e-26 of ||f||^2_G) the solutions and sigma agree to 1e-9; the first 12
+    iterates agree to round-off (before Green-Jacobi amplifies it)."""
+    rho = density(n)
+    eb = np.array([1.0, 0, 0, 0, 0, 0])
+    comm = Dm.Comm.local_ranks(P)
+    op, rhs1, rep1 = single_gpu(rho, kind, 1e-6, 999, eb)
+    D, rhs, rep = dist_solve(comm, rho, kind, 1e-6, 999, eb)
+    # rhs: same stencil arithmetic on the halo-extended slabs -> bitwise
+    assert np.array_equal(glob(rhs, P), rhs1)
+    assert rep.terminated == rep1.terminated == "converged"
+    assert abs(rep.iterations - rep1.iterations) <= 1
+    _, _, rep1 = single_gpu(rho, kind, 1e-28, 5000, eb)
+    rep = D.pcg(rhs, eta=1e-28, max_iter=5000)
+    assert rep.terminated == rep1.terminated == "converged"
+    u = glob(rep.solution, P)
+    assert rel(u, rep1.solution.values) <= 1e-9
+    sig = homogenized_stress(op, G.VectorField(op.grid, u), eb)
+    sig1 = homogenized_stress(op, rep1.solution, eb)
+    assert rel(sig, sig1) <= 1e-9
+    # fixed iterations: the whole trajectory
+    _, _, rep1 = single_gpu(rho, kind, 0.0, 12, eb)
+    rep = D.pcg(rhs, eta=0.0, max_iter=12)
+    assert rep.iterations == rep1.iterations == 12
+    assert rel(rep.residual_history, rep1.residual_history) <= 1e-11
+    assert rel(glob(rep.solution, P), rep1.solution.values) <= 1e-10
+
+
+def test_loopback_jacobi_bitwise():
+    n, P = 64, 4
+    rho = density(n, seed=5)
+    grid = G.make_grid(n, (1.0,) * 3)
+    mat = isotropic_material(LAM, MU, 3)
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    jac = assemble_jacobi(op)
+    comm = Dm.Comm.local_ranks(P)
+    D = Dm.DistSolver(comm, (n,) * 3, (1.0,) * 3, np.stack(Dm.split(rho, P, axis=1)), LAM, MU)
+    assert np.array_equal(glob(D.jacobi_inv_sqrt(), P), jac.inv_sqrt)
+
+
+def test_loopback_vs_oracle_fixed_iterations():
+    """P = 2 against the oracle: the first 10 Green-Jacobi iterates."""
+    n, P = 32, 2
+    rho = density(n, seed=7)
+    eb = ms.mandel_shear(3, 0, 1, 0.5)
+    c = X.isotropic_stiffness(3, LAM, MU)
+    h = X.pixel_size((n,) * 3, (1.0,) * 3)
+    blocks = X.assemble_green((n,) * 3, (1.0,) * 3, c)
+    inv = X.assemble_jacobi(rho, c, h)
+    f = X.assemble_rhs(rho, c, h, eb)
+    it, hist, term, x = X.pcg(rho, c, h, f, "green-jacobi", blocks, inv, eta=0.0, max_iter=10)
+    comm = Dm.Comm.local_ranks(P)
+    D, rhs, rep = dist_solve(comm, rho, "green-jacobi", 0.0, 10, eb)
+    assert rep.iterations == it == 10 and rep.terminated == "iteration-cap"
+    assert rel(rep.residual_history, hist) <= 1e-11
+    assert rel(glob(rep.solution, P), x) <= 1e-10
+
+
+def test_nccl_world1_matches_loopback():
+    n = 32
+    rho = density(n, seed=9)
+    eb = np.array([0.3, -0.2, 0.1, 0.0, 0.2, 0.5])
+    comm = Dm.Comm.nccl(Dm.unique_id(), 0, 1, 0)
+    D, rhs, rep = dist_solve(comm, rho, "green-jacobi", 1e-12, 999, eb)
+    D2, rhs2, rep2 = dist_solve(Dm.Comm.local_ranks(1), rho, "green-jacobi", 1e-12, 999, eb)
+    assert rep.iterations == rep2.iterations
+    assert rep.residual_history == rep2.residual_history
+    assert np.array_equal(rep.solution, rep2.solution[0])
+
+
+def test_dist_contract():
+    """Zero rhs -> 0 iterations; abort on NaN; cap reported."""
+    n, P = 32, 2
+    rho = density(n)
+    comm = Dm.Comm.local_ranks(P)
+    D = Dm.DistSolver(comm, (n,) * 3, (1.0,) * 3, np.stack(Dm.split(rho, P, axis=1)), LAM, MU)
+    z = np.zeros(D.local_shape)
+    rep = D.pcg(z)
+    assert rep.iterations == 0 and rep.residual_history == [0.0] and rep.terminated == "converged"
+    rhs = D.assemble_rhs(np.array([1.0, 0, 0, 0, 0, 0]))
+    rep = D.pcg(rhs, eta=0.0, max_iter=3)
+    assert rep.terminated == "iteration-cap" and rep.iterations == 3 and len(rep.residual_history) == 4
+    bad = rhs.copy()
+    bad[0, 0, 0, 0, 0] = np.nan
+    with pytest.raises(Dm.N.SolverAbortError):
+        D.pcg(bad)
+    with pytest.raises(ValueError):
+        Dm.DistSolver(Dm.Comm.local_ranks(3), (n,) * 3, (1.0,) * 3,
+                      np.stack(Dm.split(rho[:, :30], 3, axis=1)), LAM, MU)
