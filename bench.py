@@ -54,8 +54,8 @@ def parse():
                     help="PCG iterations per step (SURVEY 8d throughput mode: 50 at 512^3)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--slab", action="store_true",
-                    help="use the slab-decomposed solver even at N = 1 (testing)")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the distributed (slab) library path even at N = 1")
     return ap.parse_args()
 
 
@@ -359,31 +359,35 @@ def weak_shape(n, world):
     return tuple(shape)
 
 
-def run_slab(args, rank, world):
-    """N > 1: the slab-decomposed solver (paper_2508_02613_b200.slab), NCCL
-    halo / all-to-all / rank-ordered reductions, weak scaling."""
+def run_dist(args, rank, world):
+    """N > 1 (or --dist): the slab-decomposed solver inside libjfftb200
+    (csrc/dist.cu via paper_2508_02613_b200.dist): fused passes per rank,
+    NCCL halo rows / all-to-all / all-gathers on the solver's stream, device
+    scalars; weak scaling (the 512^3 cell per GPU)."""
     import torch
     import torch.distributed as dist
     from paper_2508_02613_b200 import _native as N
+    from paper_2508_02613_b200 import dist as Dm
     from paper_2508_02613_b200 import microstructures as ms
     from paper_2508_02613_b200 import roofline as R
-    from paper_2508_02613_b200.slab import DeviceBackend, SlabLayout, SlabPCG
     d, n, gen, eb = WORKLOADS[args.workload]
     assert d == 3, "slab decomposition is 3-D; 2-D runs as replicas"
     shape = weak_shape(n, world)
     lengths = tuple(k / n for k in shape)  # same pixel size as the 1-GPU cell
-    lay = SlabLayout(shape, lengths, world, rank)
     dev = torch.device("cuda", torch.cuda.current_device())
     lam, mu = ms.lame_from_poisson()
     count = int(round(64 * (shape[0] * shape[1] * shape[2]) / 512 ** 3))
-    rho = ms.crack_discs_device(shape, count=count, seed=0, device=dev,
-                                planes=(lay.plane0, lay.plane0 + lay.L0))
-    solver = SlabPCG(lay, DeviceBackend(dev), rho, lam, mu, kind=args.kind)
-    rhs = solver.assemble_rhs(np.asarray(eb, dtype=np.float64))
+    lo, hi = Dm.slab_rows(shape[1], world, rank)
+    rho = ms.crack_discs_device(shape, count=count, seed=0, device=dev, rows=(lo, hi))
+    comm = Dm.Comm.nccl_from_torch()
+    solver = Dm.DistSolver(comm, shape, lengths, rho.contiguous(), lam, mu, kind=args.kind)
+    del rho
+    rhs = solver.assemble_rhs(np.asarray(eb, dtype=np.float64), device=torch.empty(1, device=dev))
+    x = torch.empty_like(rhs)
     torch.cuda.synchronize()
 
     def step():
-        solver.solve(rhs, eta=-1.0, max_iter=args.iters)
+        solver.pcg(rhs, eta=-1.0, max_iter=args.iters, x_out=x)
 
     for _ in range(args.warmup):
         step()
@@ -411,10 +415,11 @@ def run_slab(args, rank, world):
     per_iter_ms = ms_total / iters_total
     alg = R.algorithmic_bytes(args.kind, 3, Ng // world)  # per GPU
     ach = alg / (per_iter_ms / 1e3) / 1e9
-    roof = {"bound": "hbm", "kernel": "pcg-iteration (slab, per GPU)", "achieved": ach,
+    roof = {"bound": "hbm", "kernel": "pcg-iteration (distributed, per GPU)", "achieved": ach,
             "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
             "alg_bytes_per_launch": alg, "ms_per_launch": per_iter_ms, "peak_source": peak_src}
-    # e2e: the rhs from pinned host memory and the solution back, every step
+    # e2e: the rhs from pinned host memory and the solution back, every step,
+    # through the same public call with host buffers
     rhs_h = torch.empty(rhs.shape, dtype=torch.float64, pin_memory=True)
     rhs_h.copy_(rhs)
     x_h = torch.empty_like(rhs_h, pin_memory=True)
@@ -422,16 +427,14 @@ def run_slab(args, rank, world):
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(max(args.e2e_steps, 1)):
-        rhs.copy_(rhs_h, non_blocking=True)
-        _, _, _, x, _ = solver.solve(rhs, eta=-1.0, max_iter=args.iters)
-        x_h.copy_(x)
-    torch.cuda.synchronize()
+        solver.pcg(rhs_h.numpy(), eta=-1.0, max_iter=args.iters, x_out=x_h.numpy())
     te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_v = 3 * Ng * args.iters * max(args.e2e_steps, 1) / float(te.item()) / 1e9
     cfg = config_of(args)
-    cfg.update({"shape": list(shape), "parallelism": f"slab{world} (axis-0 slabs, NCCL halo + "
-                "all-to-all + allgather)", "nodes_per_gpu": Ng // world})
+    cfg.update({"shape": list(shape), "parallelism": f"slab{world} (axis-1 real slabs / k0 "
+                "spectral slabs in libjfftb200; NCCL halo rows + all-to-all + all-gather)",
+                "nodes_per_gpu": Ng // world})
     return {
         "metric": metric_name(args), "value": value, "unit": "GDOF-it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
@@ -513,13 +516,13 @@ def main():
     os.environ["JFFTB_DEVICE"] = str(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if (world > 1 or args.slab) and WORKLOADS[args.workload][0] == 3:
+    if (world > 1 or args.dist) and WORKLOADS[args.workload][0] == 3:
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
             dist.init_process_group("nccl", rank=0, world_size=1,
                                     device_id=torch.device("cuda", local))
-        line = run_slab(args, rank, world)
+        line = run_dist(args, rank, world)
     else:
         line = run_ours(args, rank, world)
     if rank == 0:

@@ -146,17 +146,6 @@ int jfftb_homogenized_stress(jfftb_op* op, const double* u, const double* eps_ba
 int jfftb_green_create(jfftb_grid* g, double lambda_ref, double mu_ref,
                        jfftb_green** out);
 int jfftb_green_destroy(jfftb_green* green);
-/* Distributed (slab-decomposed) solves, 3-D only: the Green blocks of the
- * axis-1 frequency slab k1 in [k1_lo, k1_lo + k1_count) of the rfftn half
- * spectrum, frequencies ordered (k0, k1 - k1_lo, k2), k2 = 0..n2/2. */
-int jfftb_green_create_slab(jfftb_grid* g, double lambda_ref, double mu_ref, int k1_lo,
-                            int k1_count, jfftb_green** out);
-/* Block solve on a device spectrum in that slab order (d x nfreq complex per
- * field): kind JFFTB_PC_GREEN: spec = r^, r^ <- G r^ / N;
- * kind JFFTB_PC_GREEN_JACOBI: spec = [r^ ; s^], s^ <- G s^ / N.  sums (host,
- * 2 doubles) receive this slab's Parseval-weighted r^H G r / N and
- * s^H G s / N (= the first for green). */
-int jfftb_green_slab_apply(jfftb_green* green, int kind, double* spec, double* sums);
 /* GreenOperator.blocks: host array (n0, ..., n_{d-1}/2+1, d, d) complex */
 int jfftb_green_export_blocks(jfftb_green* green, double* out);
 /* apply_green (preconditioners.py:83) */

@@ -55,9 +55,6 @@ _SIGS = {
     "jfftb_residual_force": (C.c_int, [_P, _P, _D, _P, C.c_int]),
     "jfftb_homogenized_stress": (C.c_int, [_P, _P, _D, _D, C.c_int]),
     "jfftb_green_create": (C.c_int, [_P, C.c_double, C.c_double, C.POINTER(_P)]),
-    "jfftb_green_create_slab": (C.c_int, [_P, C.c_double, C.c_double, C.c_int, C.c_int,
-                                          C.POINTER(_P)]),
-    "jfftb_green_slab_apply": (C.c_int, [_P, C.c_int, _P, _D]),
     "jfftb_green_destroy": (C.c_int, [_P]),
     "jfftb_green_export_blocks": (C.c_int, [_P, _P]),
     "jfftb_apply_green": (C.c_int, [_P, _P, _P, C.c_int]),
@@ -218,26 +215,6 @@ class GreenHandle(_Handle):
         check(load().jfftb_green_create(grid.ptr, float(lam), float(mu), C.byref(out)))
         super().__init__(out)
         self.grid = grid
-
-
-class GreenSlabHandle(_Handle):
-    """Green blocks of an axis-1 frequency slab (distributed solves)."""
-
-    _destroy = "jfftb_green_destroy"
-
-    def __init__(self, grid: GridHandle, lam, mu, k1_lo: int, k1_count: int):
-        out = C.c_void_p()
-        check(load().jfftb_green_create_slab(grid.ptr, float(lam), float(mu), int(k1_lo),
-                                             int(k1_count), C.byref(out)))
-        super().__init__(out)
-        self.grid = grid
-
-    def apply(self, kind_code: int, spec_ptr: int):
-        """In-place block solve of a device spectrum; returns (q_r, q_s)."""
-        sums = np.zeros(2)
-        check(load().jfftb_green_slab_apply(self.ptr, kind_code, C.c_void_p(spec_ptr),
-                                            dptr(sums)))
-        return float(sums[0]), float(sums[1])
 
 
 class JacobiHandle(_Handle):

@@ -698,21 +698,10 @@ int jfftb_homogenized_stress(jfftb_op* op, const double* u, const double* eps_ba
 }
 
 int jfftb_green_create(jfftb_grid* g, double lambda_ref, double mu_ref, jfftb_green** out) {
-  return jfftb_green_create_slab(g, lambda_ref, mu_ref, -1, 0, out);
-}
-
-int jfftb_green_create_slab(jfftb_grid* g, double lambda_ref, double mu_ref, int k1_lo,
-                            int k1_count, jfftb_green** out) {
   return guarded([&] {
     require(g != nullptr && out != nullptr, "null argument");
     require(mu_ref > 0.0 && lambda_ref + mu_ref > 0.0,
             "stiffness not positive definite");
-    const bool slab = k1_lo >= 0;
-    if (slab) {
-      require(g->geo.d == 3, "frequency slabs are 3-D only");
-      require(k1_count > 0 && k1_count < 2048 && k1_lo + k1_count <= g->geo.n[1],
-              "invalid axis-1 frequency slab");
-    }
     DeviceGuard dg(g->device);
     const Geom& geo = g->geo;
     // impulse responses of K_ref (rho = 1) on a small periodic grid that has
@@ -743,44 +732,18 @@ int jfftb_green_create_slab(jfftb_grid* g, double lambda_ref, double mu_ref, int
     gr->lambda_ref = lambda_ref;
     gr->mu_ref = mu_ref;
     const int np = green_planes(d);
-    const int64_t nfreq =
-        slab ? (int64_t)geo.n[0] * k1_count * geo.nh : spec_elems(g);
+    const int64_t nfreq = spec_elems(g);
     gr->nfreq = nfreq;
-    gr->slab_lo = slab ? k1_lo : -1;
-    gr->slab_cnt = slab ? k1_count : 0;
     if (cudaMalloc(&gr->blocks, sizeof(double) * np * nfreq) != cudaSuccess) {
       delete gr;
       throw Error(JFFTB_ECUDA, "cudaMalloc failed for Green blocks");
     }
-    const int layout = slab ? 2 + (k1_lo | (k1_count << 20)) : (g->fused ? 1 : 0);
+    const int layout = g->fused ? 1 : 0;
     launch_green_setup(geo, g->stream, resp.as<double>(), m[0] | (m[1] << 8) | (m[2] << 16),
                        gr->blocks, layout, nfreq, layout == 1 && fused_dif());
     JF_CUDA(cudaStreamSynchronize(g->stream));
     g->refs.fetch_add(1);
     *out = gr;
-  });
-}
-
-int jfftb_green_slab_apply(jfftb_green* green, int kind, double* spec, double* sums) {
-  return guarded([&] {
-    require(green != nullptr && spec != nullptr && sums != nullptr, "null argument");
-    require(green->slab_lo >= 0, "not a frequency-slab Green operator");
-    require(kind == JFFTB_PC_GREEN || kind == JFFTB_PC_GREEN_JACOBI,
-            "slab block solve supports the green and green-jacobi kinds");
-    jfftb_grid* g = green->grid;
-    DeviceGuard dg(g->device);
-    Geom geo = g->geo;
-    geo.Nh = green->nfreq;  // the kernel walks the slab's frequencies
-    double* part = ensure_partials(g, 2 * kRedBlocks + 2);
-    // a zeroed device PCG state (done = 0) lives in the grid's scalar scratch
-    PcgState* st = reinterpret_cast<PcgState*>(g->dscal + 16);
-    JF_CUDA(cudaMemsetAsync(st, 0, sizeof(PcgState), g->stream));
-    launch_pcg_spectral(geo, g->stream, kind == JFFTB_PC_GREEN ? 0 : 1, green->blocks,
-                        green->blocks, reinterpret_cast<double2*>(spec), st, part);
-    launch_sum_partials(g->stream, part, kRedBlocks, 2, part + 2 * kRedBlocks);
-    JF_CUDA(cudaMemcpyAsync(sums, part + 2 * kRedBlocks, 2 * sizeof(double),
-                            cudaMemcpyDeviceToHost, g->stream));
-    JF_CUDA(cudaStreamSynchronize(g->stream));
   });
 }
 

@@ -158,8 +158,6 @@ struct jfftb_green {
   // 3-D 9 planes (G00, G11, G22, Re/Im G01, Re/Im G02, Re/Im G12), each nfreq
   double* blocks;
   int64_t nfreq = 0;  // frequencies per plane
-  int slab_lo = -1;   // >= 0: axis-1 frequency slab (jfftb_green_create_slab)
-  int slab_cnt = 0;
 };
 
 struct jfftb_jacobi {

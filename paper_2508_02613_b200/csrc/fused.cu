@@ -976,7 +976,7 @@ GreenAna green_ana(const Geom& geo, const jfftb_green* gpc) {
   return ga;
 }
 bool use_analytic(const Geom& geo, const jfftb_green* gpc, const jfftb_green* gterm) {
-  return geo.d == 3 && green_analytic_enabled() && gpc->slab_lo < 0 &&
+  return geo.d == 3 && green_analytic_enabled() &&
          gterm->lambda_ref == gpc->lambda_ref && gterm->mu_ref == gpc->mu_ref;
 }
 

@@ -229,15 +229,6 @@ __global__ void green_setup_kernel(Geom g, const double* __restrict__ resp, int 
       q[D - 1] = (int)(rem % g.nh);
       rem /= g.nh;
       for (int a = D - 2; a >= 0; --a) { q[a] = (int)(rem % g.n[a]); rem /= g.n[a]; }
-    } else if (layout >= 2) {
-      // slab of the numpy layout: axis-1 frequencies [lo, lo + cnt), packed
-      // as layout - 2 = lo | cnt << 20 (distributed solves, slab.py)
-      const int lo = (layout - 2) & 0xfffff, cnt = (layout - 2) >> 20;
-      q[D - 1] = (int)(rem % g.nh);
-      rem /= g.nh;
-      q[1] = lo + (int)(rem % cnt);
-      rem /= cnt;
-      if (D == 3) q[0] = (int)rem;
     } else {
       for (int a = D - 1; a >= 1; --a) { q[a] = (int)(rem % g.n[a]); rem /= g.n[a]; }
       q[0] = (int)rem + k0_off;  // k0-slab of a distributed solve (dist.cu)

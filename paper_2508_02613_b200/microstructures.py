@@ -116,11 +116,12 @@ def crack_discs(n: int = 512, count: int = 64, ell: float = 4.0,
 
 
 def crack_discs_device(n=512, count: int = 64, ell: float = 4.0, emin: float = 1e-4,
-                       seed: int = 0, device="cuda", out=None, planes=None):
+                       seed: int = 0, device="cuda", out=None, planes=None, rows=None):
     """Device (torch) version of :func:`crack_discs` with the same seeded
     geometry, for bench-size grids.  ``n`` is an int (cubic) or a shape
-    (n0, n1, n2); ``planes = (lo, hi)`` generates only those axis-0 planes
-    (one slab of a distributed run).  Returns a float64 tensor."""
+    (n0, n1, n2); ``planes = (lo, hi)`` generates only those axis-0 planes,
+    ``rows = (lo, hi)`` only those axis-1 rows (one slab of a distributed
+    run, paper_2508_02613_b200.dist).  Returns a float64 tensor."""
     import torch
     shape = (n,) * 3 if isinstance(n, int) else tuple(int(k) for k in n)
     if isinstance(n, int):
@@ -133,13 +134,16 @@ def crack_discs_device(n=512, count: int = 64, ell: float = 4.0, emin: float = 1
         radii = rng.uniform(8.0, 32.0, count)
     lo, hi = planes if planes is not None else (0, shape[0])
     axes = [torch.arange(k, dtype=torch.float64, device=device) + 0.5 for k in shape]
-    if out is None:
-        out = torch.empty((hi - lo,) + shape[1:], dtype=torch.float64, device=device)
     n1, n2 = shape[1], shape[2]
-    chunk = max(1, min(hi - lo, (1 << 24) // (n1 * n2)))
+    r0, r1 = rows if rows is not None else (0, n1)
+    axes[1] = axes[1][r0:r1]
+    if out is None:
+        out = torch.empty((hi - lo, r1 - r0, n2), dtype=torch.float64, device=device)
+    chunk = max(1, min(hi - lo, (1 << 24) // ((r1 - r0) * n2)))
     for i0 in range(lo, hi, chunk):
         x0 = axes[0][i0:min(i0 + chunk, hi)]
-        dmin = torch.full((len(x0), n1, n2), float("inf"), dtype=torch.float64, device=device)
+        dmin = torch.full((len(x0), r1 - r0, n2), float("inf"), dtype=torch.float64,
+                          device=device)
         for c, nr, r in zip(centres, normals, radii):
             v0 = x0 - c[0]
             v0 = (v0 - shape[0] * torch.round(v0 / shape[0]))[:, None, None]
