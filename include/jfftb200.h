@@ -179,6 +179,19 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
               int max_iter, double* x_out, double* history_out, int* iterations,
               int* terminated, double* wall_s);
 
+/* pcg over nrhs right-hand sides at once (the load cases of
+ * topopt.py:98-127 share one operator and preconditioner): rhs / x_out hold
+ * nrhs vector fields back to back, history_out nrhs x (max_iter + 1),
+ * iterations / terminated nrhs entries.  Every stage is one launch for all
+ * solves (a grid dimension per right-hand side, a device PCG state each), so
+ * rho, D^-1/2 and the Green planes are read once per stage for all of them;
+ * each solve stops on its own test (solver.py semantics per solve).  Fused
+ * 3-D grids, kinds green / green-jacobi. */
+int jfftb_pcg_batch(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
+                    jfftb_green* green_term, int nrhs, const double* rhs, int where, double eta,
+                    int max_iter, double* x_out, double* history_out, int* iterations,
+                    int* terminated, double* wall_s);
+
 /* ---- device-side stage profile (no reference counterpart; SolveReport's
  * wall_time, solver.py:88,139, is the reference's only timing) ----------- */
 #define JFFTB_N_STAGES 8  /* stencil, alpha, update, fft_fwd, spectral,

@@ -74,6 +74,8 @@ _SIGS = {
     "jfftb_simp_projection": (C.c_int, [_P, _P, C.c_double, C.c_double, C.c_int]),
     "jfftb_field_layout": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int]),
     "jfftb_load_pairings": (C.c_int, [_P, C.c_int, _P, _D, _D, _D, _P, C.c_int]),
+    "jfftb_pcg_batch": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, _P, C.c_int, C.c_double,
+                                  C.c_int, _P, _D, C.POINTER(C.c_int), C.POINTER(C.c_int), _D]),
     "jfftb_comm_unique_id": (C.c_int, [C.c_char_p]),
     "jfftb_comm_create_nccl": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "jfftb_comm_create_local": (C.c_int, [C.c_int, C.c_int, C.POINTER(_P)]),

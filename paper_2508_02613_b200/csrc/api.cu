@@ -226,6 +226,56 @@ PcgBuffers pcg_workspace(jfftb_grid* g, int kcount, int max_iter) {
   return B;
 }
 
+// workspace of a batched solve (L right-hand sides; spectral kinds on the
+// fused path): per solve x, r, p, Kp (d N each), 2d spectra, state, history
+PcgBuffers pcg_workspace_batch(jfftb_grid* g, int kcount, int max_iter, int L, Batch& bt) {
+  const Geom& geo = g->geo;
+  const int64_t n = geo.d * geo.N;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const int64_t nspec = spec_elems(g);
+  const int hstride = max_iter + 1;
+  const size_t total = al(sizeof(double) * n * L) * 4 + al(sizeof(double2) * 2 * geo.d * nspec * L) +
+                       al(sizeof(PcgState) * L) +
+                       al(sizeof(double) * ((size_t)kcount * L + 2 * kFusedMaxBlocks + kRedBlocks)) +
+                       al(sizeof(double) * hstride * L);
+  if (g->wsb_bytes < total) {
+    if (g->wsb) JF_CUDA(cudaFree(g->wsb));
+    g->wsb = nullptr;
+    g->wsb_bytes = 0;
+    JF_CUDA(cudaMalloc(&g->wsb, total));
+    g->wsb_bytes = total;
+  }
+  if (g->wsb_L < L) {
+    if (g->wsb_host) JF_CUDA(cudaFreeHost(g->wsb_host));
+    g->wsb_host = nullptr;
+    JF_CUDA(cudaMallocHost(&g->wsb_host, sizeof(PcgState) * L));
+    g->wsb_L = L;
+  }
+  char* p = static_cast<char*>(g->wsb);
+  auto take = [&](size_t b) {
+    char* q = p;
+    p += al(b);
+    return q;
+  };
+  PcgBuffers B{};
+  B.x = (double*)take(sizeof(double) * n * L);
+  B.rs = (double*)take(sizeof(double) * n * L);
+  B.p = (double*)take(sizeof(double) * n * L);
+  B.kp = (double*)take(sizeof(double) * n * L);
+  B.spec = (double2*)take(sizeof(double2) * 2 * geo.d * nspec * L);
+  B.st = (PcgState*)take(sizeof(PcgState) * L);
+  B.kpart = (double*)take(sizeof(double) * ((size_t)kcount * L + 2 * kFusedMaxBlocks + kRedBlocks));
+  B.spart = B.kpart + (size_t)kcount * L;
+  B.upart = B.spart + 2 * kFusedMaxBlocks;
+  B.kcount = kcount;
+  B.hist = (double*)take(sizeof(double) * hstride * L);
+  B.hstride = hstride;
+  bt.L = L;
+  bt.vs = n;
+  bt.bss = 2 * geo.d * nspec;
+  return B;
+}
+
 bool graphs_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("JFFTB_GRAPHS");
@@ -469,6 +519,8 @@ void grid_free(jfftb_grid* g) {
     if (g->dscal) cudaFree(g->dscal);
     if (g->ws) cudaFree(g->ws);
     if (g->ws_host) cudaFreeHost(g->ws_host);
+    if (g->wsb) cudaFree(g->wsb);
+    if (g->wsb_host) cudaFreeHost(g->wsb_host);
     if (g->twiddle) cudaFree(g->twiddle);
     free_host_staging(g);
     drop_iteration_graph(g);
@@ -999,6 +1051,87 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
         copy_d2h(g, x_out, B.x, sizeof(double) * n, s);
       else
         JF_CUDA(cudaMemcpyAsync(x_out, B.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    }
+    JF_CUDA(cudaStreamSynchronize(s));
+    if (wall_s)
+      *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int jfftb_pcg_batch(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
+                    jfftb_green* green_term, int nrhs, const double* rhs, int where, double eta,
+                    int max_iter, double* x_out, double* history_out, int* iterations,
+                    int* terminated, double* wall_s) {
+  const auto t0 = std::chrono::steady_clock::now();
+  return guarded([&] {
+    require(op != nullptr && green_term != nullptr, "pcg needs an operator and a Green operator");
+    require(rhs && history_out && iterations && terminated, "null argument");
+    require(nrhs >= 1 && nrhs <= 64, "1 to 64 right-hand sides");
+    require(max_iter >= 0, "max_iter must be >= 0");
+    require(where == JFFTB_HOST || where == JFFTB_DEVICE, "where must be HOST or DEVICE");
+    jfftb_grid* g = op->grid;
+    require(g->fused && g->geo.d == 3 &&
+                (kind == JFFTB_PC_GREEN || kind == JFFTB_PC_GREEN_JACOBI),
+            "batched solves run the fused 3-D spectral kinds (use jfftb_pcg otherwise)");
+    require(green_term->grid == g && green_pc != nullptr && green_pc->grid == g,
+            "Green operators live on a different grid");
+    if (kind == JFFTB_PC_GREEN_JACOBI)
+      require(jac != nullptr && jac->op->grid == g, "kind needs an assembled Jacobi diagonal");
+    DeviceGuard dg(g->device);
+    const Geom& geo = g->geo;
+    cudaStream_t s = g->stream;
+    const int64_t n = geo.d * geo.N;
+    Batch bt;
+    PcgBuffers B = pcg_workspace_batch(g, stencil_blocks(geo), max_iter, nrhs, bt);
+    PcgState* hs = g->wsb_host;
+    for (int l = 0; l < nrhs; ++l) {
+      PcgState h0{};
+      h0.eta = eta;
+      h0.max_iter = max_iter;
+      hs[l] = h0;
+    }
+    JF_CUDA(cudaMemcpyAsync(B.st, hs, sizeof(PcgState) * nrhs, cudaMemcpyHostToDevice, s));
+    JF_CUDA(cudaMemsetAsync(B.x, 0, sizeof(double) * n * nrhs, s));
+    if (where == JFFTB_HOST)
+      copy_h2d(g, B.rs, rhs, sizeof(double) * n * nrhs, s);
+    else
+      JF_CUDA(cudaMemcpyAsync(B.rs, rhs, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, s));
+    auto poll = [&]() {
+      JF_CUDA(cudaMemcpyAsync(hs, B.st, sizeof(PcgState) * nrhs, cudaMemcpyDeviceToHost, s));
+      JF_CUDA(cudaStreamSynchronize(s));
+      for (int l = 0; l < nrhs; ++l)
+        if (!hs[l].done) return false;
+      return true;
+    };
+    pcg_dispatch_batch(kind, true, op, jac, green_pc, green_term, B, bt);
+    bool done = poll();
+    int batch = 1;
+    while (!done) {
+      for (int k = 0; k < batch; ++k)
+        pcg_dispatch_batch(kind, false, op, jac, green_pc, green_term, B, bt);
+      done = poll();
+      batch = std::min(batch * 2, 8);
+    }
+    int status = JFFTB_OK;
+    for (int l = 0; l < nrhs; ++l) {
+      iterations[l] = hs[l].iters;
+      terminated[l] = hs[l].gnorm2 <= eta ? JFFTB_CONVERGED : JFFTB_ITERATION_CAP;
+      JF_CUDA(cudaMemcpyAsync(history_out + (size_t)l * (max_iter + 1), B.hist + (size_t)l * B.hstride,
+                              sizeof(double) * (hs[l].iters + 1), cudaMemcpyDeviceToHost, s));
+      if (hs[l].status != JFFTB_OK && status == JFFTB_OK) status = hs[l].status;
+    }
+    JF_CUDA(cudaStreamSynchronize(s));
+    if (status != JFFTB_OK)
+      throw Error(status, status == JFFTB_ECURVATURE
+                              ? "non-positive search-direction curvature in PCG"
+                              : "PCG recurrence became non-finite");
+    double* part = ensure_partials(g, kRedBlocks * 3 + 3);
+    for (int l = 0; l < nrhs; ++l) launch_sub_mean(geo, s, B.x + (size_t)l * n, part);
+    if (x_out) {
+      if (where == JFFTB_HOST)
+        copy_d2h(g, x_out, B.x, sizeof(double) * n * nrhs, s);
+      else
+        JF_CUDA(cudaMemcpyAsync(x_out, B.x, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, s));
     }
     JF_CUDA(cudaStreamSynchronize(s));
     if (wall_s)

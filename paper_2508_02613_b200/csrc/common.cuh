@@ -124,9 +124,13 @@ struct jfftb_grid {
   // fused spectral path (fused.cu): power-of-two grids, 16 <= n <= 2048
   bool fused = false;
   double2* twiddle = nullptr;   // exp(-2 pi i j / 4096)
-  // cached PCG workspace (api.cu pcg_workspace)
+  // cached PCG workspace (api.cu pcg_workspace) and the batched one
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  void* wsb = nullptr;
+  size_t wsb_bytes = 0;
+  jfftb::PcgState* wsb_host = nullptr;
+  int wsb_L = 0;
   jfftb::PcgState* ws_host = nullptr;  // pinned mirror of the device state
   // stage profile (jfftb_profile_*)
   bool prof = false;
@@ -314,6 +318,11 @@ int launch_stencil(const Geom& g, cudaStream_t s, int mode, const double* u,
                    const double* rho, double lam, double mu, const double* ebar_mandel,
                    double* out, double* curv_partials, int ext = 0);
 int stencil_blocks(const Geom& g);
+// K u for nb right-hand sides bstride doubles apart (one launch; returns the
+// partials per right-hand side, rhs b's at curv_partials + b * that)
+int launch_stencil_batch(const Geom& g, cudaStream_t s, const double* u, const double* rho,
+                         double lam, double mu, double* out, double* curv_partials, int nb,
+                         int64_t bstride);
 
 void launch_total_strain(const Geom& g, cudaStream_t s, const double* u,
                          const double* ebar, double* out);
@@ -402,9 +411,18 @@ struct PcgBuffers {
   double* hist;
   double *kpart, *spart, *upart;
   int kcount;
+  int hstride = 0;          // batched: history entries per right-hand side
+};
+// batched right-hand sides: L solves, vector fields vs doubles apart,
+// spectra bss complex elements apart (L = 1: the plain solve)
+struct Batch {
+  int L = 1;
+  int64_t vs = 0, bss = 0;
 };
 void pcg_dispatch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
                   jfftb_green* gterm, const PcgBuffers& B);
+void pcg_dispatch_batch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
+                        jfftb_green* gterm, const PcgBuffers& B, const Batch& bt);
 
 // fused spectral path (fused.cu)
 bool fused_supported(const Geom& g);
@@ -422,17 +440,18 @@ void fused_precond_apply(const Geom& geo, cudaStream_t s, const jfftb_green* gre
                          const double* dinv, const double* r, double* out, double2* spec,
                          const double2* tw);
 enum { FUSED_APPLY = 0, FUSED_INIT = 1, FUSED_ITER = 2 };
+struct Batch;
 void fused_stage_A(const Geom& geo, cudaStream_t s, int F, int mode, const PcgState* st,
                    double* r, const double* kp, const double* dinv, double2* spec,
-                   const double2* tw);
+                   const double2* tw, const Batch& bt);
 void fused_stage_B(const Geom& geo, cudaStream_t s, bool inv, const PcgState* st,
-                   double2* spec, int ncomp, const double2* tw);
+                   double2* spec, int ncomp, const double2* tw, const Batch& bt);
 int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const PcgState* st,
                   const jfftb_green* gpc, const jfftb_green* gterm, double2* spec,
-                  double* partials, const double2* tw);
+                  double* partials, const double2* tw, const Batch& bt);
 void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                    const double2* zspec, const double* dinv, double* p, double* x,
-                   const double2* tw);
+                   const double2* tw, const Batch& bt);
 int64_t fused_component_stride(const Geom& geo);
 // distributed solves (dist.cu): one rank's k0-slab of the spectral passes
 struct SpecSlab {

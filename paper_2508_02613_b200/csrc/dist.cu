@@ -292,7 +292,8 @@ void run_p2p(jfftb_dist* D, const std::vector<P2P>& xs) {
   cudaStream_t s = D->stream;
   if (c->local) {
     for (const auto& x : xs)
-      if (x.bytes) JF_CUDA(cudaMemcpyAsync(x.dst, x.src, x.bytes, cudaMemcpyDeviceToDevice, s));
+      if (x.bytes && x.src != x.dst)
+        JF_CUDA(cudaMemcpyAsync(x.dst, x.src, x.bytes, cudaMemcpyDeviceToDevice, s));
     return;
   }
   const NcclApi& N = nccl();
@@ -300,7 +301,8 @@ void run_p2p(jfftb_dist* D, const std::vector<P2P>& xs) {
   for (const auto& x : xs) {
     if (!x.bytes) continue;
     if (x.from == c->rank && x.to == c->rank) {
-      JF_CUDA(cudaMemcpyAsync(x.dst, x.src, x.bytes, cudaMemcpyDeviceToDevice, s));
+      if (x.src != x.dst)
+        JF_CUDA(cudaMemcpyAsync(x.dst, x.src, x.bytes, cudaMemcpyDeviceToDevice, s));
     } else if (x.from == c->rank) {
       JF_NCCL(N.Send(x.src, x.bytes, ncclUint8, x.to, c->nc, s));
     } else if (x.to == c->rank) {
@@ -419,7 +421,8 @@ void precond_phase(jfftb_dist* D, bool init) {
   cudaStream_t s = D->stream;
   const int mode = init ? FUSED_INIT : FUSED_ITER;
   for (auto& rk : D->ranks)
-    fused_stage_A(D->gl, s, F, mode, rk.st, rk.rs, rk.kp, GJ ? rk.dinv : nullptr, rk.spec, D->tw);
+    fused_stage_A(D->gl, s, F, mode, rk.st, rk.rs, rk.kp, GJ ? rk.dinv : nullptr, rk.spec, D->tw,
+                  Batch{});
   alltoall_fwd(D);
   for (auto& rk : D->ranks) {
     const SpecSlab sl = D->slab(rk);
@@ -595,8 +598,11 @@ int jfftb_dist_create(jfftb_comm* comm, const int64_t* n, const double* lengths,
         JF_CUDA(cudaMemsetAsync(rk.p_ext, 0, sizeof(double) * 3 * Next, D->stream));
         rk.kp = rk.alloc(sizeof(double) * 3 * Nl);
         rk.spec = reinterpret_cast<double2*>(rk.alloc(sizeof(double2) * nf * D->K0() * PSl));
-        rk.recv = reinterpret_cast<double2*>(
-            rk.alloc(sizeof(double2) * (size_t)nf * rk.kcnt * D->n[1] * D->n[2]));
+        // one rank: the received layout [src][field][k0][i1][i2] IS pass A's
+        // [field][k0][columns], so the spectra are not exchanged at all
+        rk.recv = P == 1 ? rk.spec
+                         : reinterpret_cast<double2*>(rk.alloc(
+                               sizeof(double2) * (size_t)nf * rk.kcnt * D->n[1] * D->n[2]));
         rk.green = rk.alloc(sizeof(double) * 9 * (size_t)rk.kcnt * D->n[1] * D->n[2]);
         if (!comm->local) rk.hbuf = rk.alloc(sizeof(double) * 4 * 3 * D->n[0] * D->n[2]);
         rk.part = rk.alloc(sizeof(double) * std::max(D->kcount, 2 * kFusedMaxBlocks + 8 * kRedBlocks));

@@ -70,6 +70,10 @@ struct FGeom {
   int k0lo;
   // pass I: the direction p may live in a halo-extended slab (dist.cu)
   int64_t pN, pPS, poff;
+  // batched right-hand sides (pcg_batch): L solves side by side, one PCG
+  // state each; vector fields vs doubles and spectra bss complex apart
+  int L;
+  int64_t vs, bss;
   __device__ __forceinline__ int64_t row_off(int64_t row) const {
     const int64_t k = row >> rsh;
     const int k1 = (int)(row & ((1 << rsh) - 1));
@@ -114,8 +118,12 @@ __global__ void __launch_bounds__(passA_nt(M, F, TW), passA_nt(M, F, TW) <= 512 
   static_assert(PE * NT == RAWN && PE % CH == 0, "pass A tiling");
   static_assert(F == 1 || MODE != FM_APPLY, "APPLY transforms one field");
   extern __shared__ double2 sbuf[];  // packed tile [k][field][col], k < M
+  const int c = blockIdx.y % g.d, bl = blockIdx.y / g.d;  // component, right-hand side
+  if (st) st += bl;
+  r += bl * g.vs;
+  if (kp) kp += bl * g.vs;
+  spec += bl * g.bss;
   if (MODE != FM_APPLY && st->done) return;
-  const int c = blockIdx.y;
   const int64_t col0 = (int64_t)blockIdx.x * TW;
   const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
   double* rc = r + c * g.N + col0;
@@ -203,8 +211,12 @@ __global__ void __launch_bounds__(passA3_nt<M>(), 1)
   constexpr int Q0 = M / R0;
   static_assert(MODE == FM_ITER || MODE == FM_INIT, "pass A3 runs the PCG modes");
   extern __shared__ double2 sbuf[];   // [m][field][col]
+  const int c = blockIdx.y % g.d, bl = blockIdx.y / g.d;  // component, right-hand side
+  st += bl;
+  r += bl * g.vs;
+  kp += bl * g.vs;
+  spec += bl * g.bss;
   if (st->done) return;
-  const int c = blockIdx.y;
   const int64_t col0 = (int64_t)blockIdx.x * TW;
   const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
   const int col = threadIdx.x % TW, j = threadIdx.x / TW;
@@ -326,12 +338,15 @@ __global__ void __launch_bounds__(passA3_nt<M>(), 1)
 template <int L, bool INV, bool PRED, bool SEG>
 __global__ void __launch_bounds__(nt_for(tw_b(L) * L / 8))
     passB(FGeom g, const PcgState* __restrict__ st, double2* __restrict__ spec, int comp0,
-          int nlast, const double2* __restrict__ tw) {
+          int ncomp, const double2* __restrict__ tw) {
   constexpr int TW = tw_b(L);
   constexpr int NT = nt_for(TW * L / 8);
   extern __shared__ double2 sbuf[];  // [i1][col]
+  const int nlast = g.nlast;
+  const int c = comp0 + (int)blockIdx.z % ncomp, bl = (int)blockIdx.z / ncomp;
+  if (st) st += bl;
+  spec += bl * g.bss;
   if (PRED && st->done) return;
-  const int c = comp0 + blockIdx.z;
   const int k0 = blockIdx.y;
   const int64_t col0 = (int64_t)blockIdx.x * TW;
   double2* base = spec + c * g.FS + (int64_t)k0 * g.KS + col0;
@@ -536,6 +551,9 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
   // [ rows: NQ x RL double2 | Green planes: GP x L double ]
   extern __shared__ double2 sbuf[];
   __shared__ double red[64];
+  if (st) st += blockIdx.y;  // right-hand side
+  spec += blockIdx.y * g.bss;
+  if (partials) partials += 2 * (int64_t)gridDim.x * blockIdx.y;
   if (MODE != FM_APPLY && st->done) return;
   static_assert(MODE != FM_QUAD || F == 1, "quad-only pass holds one spectrum");
   const double invN = 1.0 / (double)g.N;
@@ -688,9 +706,13 @@ __global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
   constexpr int TW = tw_a(M);
   constexpr int NT = passI_nt(M);
   extern __shared__ double2 sbuf[];  // [k][col], k <= M
+  const int c = blockIdx.y % g.d, bl = blockIdx.y / g.d;  // component, right-hand side
+  if (st) st += bl;
+  zspec += bl * g.bss;
+  if (p) p += bl * g.vs;
+  if (x) x += bl * g.vs;
   if (MODE == FM_ITER && !st->xupd) return;
   if (MODE == FM_INIT && st->done) return;
-  const int c = blockIdx.y;
   const int64_t col0 = (int64_t)blockIdx.x * TW;
   const double2* zc = zspec + c * g.CS + col0;
   for (int e = threadIdx.x; e < (M + 1) * TW; e += NT) {
@@ -780,6 +802,9 @@ FGeom fgeom(const Geom& g) {
   f.pN = f.N;
   f.pPS = f.PS;
   f.poff = 0;
+  f.L = 1;
+  f.vs = 0;
+  f.bss = 0;
   return f;
 }
 
@@ -792,7 +817,7 @@ void launchA_MT(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, c
   auto k = passA<M, F, MODE, TW>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  dim3 grid((unsigned)(g.PS / TW), g.d);
+  dim3 grid((unsigned)(g.PS / TW), g.d * g.L);
   k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
   JF_LAUNCHED();
 }
@@ -823,7 +848,7 @@ void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, co
       auto k = passA3_fused_last() ? passA3<M, MODE, true> : passA3<M, MODE, false>;
       static std::atomic<uint64_t> attr{0};
       set_smem_once(k, smem, attr);
-      dim3 grid((unsigned)(g.PS / TW), g.d);
+      dim3 grid((unsigned)(g.PS / TW), g.d * g.L);
       k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
       JF_LAUNCHED();
       return;
@@ -840,8 +865,8 @@ void launchB_L(const FGeom& g, cudaStream_t s, const PcgState* st, double2* spec
   auto k = g.SS != 0 ? passB<L, INV, PRED, true> : passB<L, INV, PRED, false>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  dim3 grid((unsigned)(g.nlast / TW), g.K0, ncomp);
-  k<<<grid, NT, smem, s>>>(g, st, spec, comp0, g.nlast, tw);
+  dim3 grid((unsigned)(g.nlast / TW), g.K0, ncomp * g.L);
+  k<<<grid, NT, smem, s>>>(g, st, spec, comp0, ncomp, tw);
   JF_LAUNCHED();
 }
 template <int D, int L, int F, int MODE, int GS, bool IP>
@@ -860,8 +885,10 @@ int launchC_V(const FGeom& g, cudaStream_t s, const PcgState* st, const double* 
   }
   const int per_sm = per_sm_dev[dev];
   const int64_t rows = g.CS / L;
-  const int blocks = (int)std::min<int64_t>(rows, (int64_t)std::max(per_sm, 1) * 148 * 4);
-  k<<<blocks, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, ga);
+  // batched right-hand sides share the grid's blocks (the rows of one Green
+  // plane set are read by L CTAs at about the same time: L2 hits)
+  const int blocks = (int)std::min<int64_t>(rows, (int64_t)std::max(per_sm, 1) * 148 * 4 / g.L);
+  k<<<dim3(blocks, g.L), NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, ga);
   JF_LAUNCHED();
   return blocks;
 }
@@ -899,7 +926,7 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
   auto k = passI<M, MODE>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  dim3 grid((unsigned)(g.PS / TW), g.d);
+  dim3 grid((unsigned)(g.PS / TW), g.d * g.L);
   k<<<grid, NT, smem, s>>>(g, st, zspec, dinv, p, x, out, tw);
   JF_LAUNCHED();
 }
@@ -1039,21 +1066,28 @@ void fused_debug_apply(const Geom& geo, cudaStream_t s, const jfftb_green* green
 // ---- the PCG stages (pcg.cu strings them together) ------------------------
 // A: mode FUSED_INIT / FUSED_ITER with F = 1 (green) or 2 (green-jacobi);
 //    FUSED_APPLY transforms r (dinv == null) for the quad-only termination
+FGeom fgeom_b(const Geom& geo, const Batch& bt) {
+  FGeom g = fgeom(geo);
+  g.L = bt.L;
+  g.vs = bt.vs;
+  g.bss = bt.bss;
+  return g;
+}
 void fused_stage_A(const Geom& geo, cudaStream_t s, int F, int mode, const PcgState* st,
                    double* r, const double* kp, const double* dinv, double2* spec,
-                   const double2* tw) {
-  launchA(fgeom(geo), s, F, mode, st, r, kp, dinv, spec, tw);
+                   const double2* tw, const Batch& bt) {
+  launchA(fgeom_b(geo, bt), s, F, mode, st, r, kp, dinv, spec, tw);
 }
 void fused_stage_B(const Geom& geo, cudaStream_t s, bool inv, const PcgState* st,
-                   double2* spec, int ncomp, const double2* tw) {
-  const FGeom g = fgeom(geo);
+                   double2* spec, int ncomp, const double2* tw, const Batch& bt) {
+  const FGeom g = fgeom_b(geo, bt);
   if (g.d == 3) launchB(g, s, inv, true, st, spec, 0, ncomp, tw);
 }
-// returns the number of partial pairs written
+// returns the number of partial pairs written (per right-hand side)
 int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const PcgState* st,
                   const jfftb_green* gpc_h, const jfftb_green* gterm_h, double2* spec,
-                  double* partials, const double2* tw) {
-  const FGeom g = fgeom(geo);
+                  double* partials, const double2* tw, const Batch& bt) {
+  const FGeom g = fgeom_b(geo, bt);
   const double* gpc = gpc_h->blocks;
   const double* gterm = gterm_h->blocks;
   const GreenAna ga = green_ana(geo, gpc_h);
@@ -1071,8 +1105,8 @@ int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const 
 }
 void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                    const double2* zspec, const double* dinv, double* p, double* x,
-                   const double2* tw) {
-  launchI(fgeom(geo), s, mode, st, zspec, dinv, p, x, nullptr, tw);
+                   const double2* tw, const Batch& bt) {
+  launchI(fgeom_b(geo, bt), s, mode, st, zspec, dinv, p, x, nullptr, tw);
 }
 int64_t fused_component_stride(const Geom& geo) { return fgeom(geo).CS; }
 

@@ -42,9 +42,12 @@ __device__ double sum_strided(const double* p, int count, int stride, int j, dou
   return s;  // valid in thread 0
 }
 
+// one block per right-hand side (blockIdx.x); pb: partials between them
 __global__ void alpha_kernel(PcgState* st, const double* __restrict__ partials, int count,
-                             int stride) {
+                             int stride, int64_t pb) {
   __shared__ double red[32];
+  st += blockIdx.x;
+  partials += blockIdx.x * pb;
   if (st->done) {
     if (threadIdx.x == 0) st->xupd = 0;
     return;
@@ -103,8 +106,12 @@ __global__ void __launch_bounds__(256)
 template <int KIND, bool INIT>
 __global__ void finalize_kernel(PcgState* st, const double* __restrict__ spart, int scount,
                                 int sstride, const double* __restrict__ upart, int ucount,
-                                double* __restrict__ hist) {
+                                double* __restrict__ hist, int64_t sb = 0, int hb = 0) {
   __shared__ double red[32];
+  // one block per right-hand side: sb partials, hb history entries apart
+  st += blockIdx.x;
+  spart += blockIdx.x * sb;
+  hist += (int64_t)blockIdx.x * hb;
   if (st->done) return;
   const double q0 = sum_strided(spart, scount, sstride, 0, red);
   const double q1 = sum_strided(spart, scount, sstride, 1, red);
@@ -232,20 +239,21 @@ static void pcg_precond_phase_fused(jfftb_grid* g, jfftb_jacobi* jac, jfftb_gree
   int scount;
   if (SPECTRAL_PC) {
     // r' = r - alpha Kp and its transform; green-jacobi adds s = D^-1/2 r'
-    fused_stage_A(geo, s, F, INIT ? FUSED_INIT : FUSED_ITER, B.st, r, B.kp, dinv, B.spec, tw);
+    fused_stage_A(geo, s, F, INIT ? FUSED_INIT : FUSED_ITER, B.st, r, B.kp, dinv, B.spec, tw,
+                  Batch{});
     if (!INIT) prof_mark(g);
-    fused_stage_B(geo, s, false, B.st, B.spec, F * geo.d, tw);
+    fused_stage_B(geo, s, false, B.st, B.spec, F * geo.d, tw, Batch{});
     if (!INIT) prof_mark(g);
-    scount = fused_stage_C(geo, s, F, false, B.st, gpc, gterm, B.spec, B.spart, tw);
+    scount = fused_stage_C(geo, s, F, false, B.st, gpc, gterm, B.spec, B.spart, tw, Batch{});
   } else {
     update_kernel<KIND, INIT><<<kRedBlocks, 256, 0, s>>>(n, B.st, B.x, r, B.p, B.kp, dinv, sz,
                                                          B.upart);
     JF_LAUNCHED();
     if (!INIT) prof_mark(g);
-    fused_stage_A(geo, s, 1, FUSED_APPLY, B.st, r, nullptr, nullptr, B.spec, tw);
-    fused_stage_B(geo, s, false, B.st, B.spec, geo.d, tw);
+    fused_stage_A(geo, s, 1, FUSED_APPLY, B.st, r, nullptr, nullptr, B.spec, tw, Batch{});
+    fused_stage_B(geo, s, false, B.st, B.spec, geo.d, tw, Batch{});
     if (!INIT) prof_mark(g);
-    scount = fused_stage_C(geo, s, 1, true, B.st, gterm, gterm, B.spec, B.spart, tw);
+    scount = fused_stage_C(geo, s, 1, true, B.st, gterm, gterm, B.spec, B.spart, tw, Batch{});
   }
   if (!INIT) prof_mark(g);
   finalize_kernel<KIND, INIT><<<1, 1024, 0, s>>>(B.st, B.spart, scount, 2, B.upart,
@@ -254,10 +262,10 @@ static void pcg_precond_phase_fused(jfftb_grid* g, jfftb_jacobi* jac, jfftb_gree
   if (!INIT) prof_mark(g);
   if (SPECTRAL_PC) {
     double2* z = B.spec + (GJ ? geo.d * fused_component_stride(geo) : 0);
-    fused_stage_B(geo, s, true, B.st, z, geo.d, tw);
+    fused_stage_B(geo, s, true, B.st, z, geo.d, tw, Batch{});
     if (!INIT) prof_mark(g);
     fused_stage_I(geo, s, INIT ? FUSED_INIT : FUSED_ITER, B.st, z, GJ ? dinv : nullptr, B.p, B.x,
-                  tw);
+                  tw, Batch{});
   } else {
     if (!INIT) prof_mark(g);
     pupdate_kernel<KIND, INIT><<<grid_n(n), 256, 0, s>>>(n, B.st, B.p,
@@ -278,7 +286,7 @@ static void pcg_iteration(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
   prof_mark(g);
   launch_stencil(g->geo, s, ST_K, B.p, op->rho, op->lambda0, op->mu0, nullptr, B.kp, B.kpart);
   prof_mark(g);
-  alpha_kernel<<<1, 1024, 0, s>>>(B.st, B.kpart, B.kcount, 1);
+  alpha_kernel<<<1, 1024, 0, s>>>(B.st, B.kpart, B.kcount, 1, 0);
   JF_LAUNCHED();
   prof_mark(g);
   if (g->fused) pcg_precond_phase_fused<KIND, false>(g, jac, gpc, gterm, B);
@@ -292,8 +300,53 @@ static void pcg_init(jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc, jfftb_gr
   else pcg_precond_phase<KIND, true>(op->grid, jac, gpc, gterm, B);
 }
 
+// ---- batched right-hand sides (jfftb_pcg_batch): the fused passes of the
+// spectral kinds with one launch per stage for all L solves (grid dimension
+// per right-hand side, per-solve device state); rho, D^-1/2 and the Green
+// planes are shared by the L solves of a launch
+template <int KIND, bool INIT>
+static void pcg_phase_batch(jfftb_grid* g, jfftb_jacobi* jac, jfftb_green* gpc, jfftb_green* gterm,
+                            const PcgBuffers& B, const Batch& bt) {
+  const Geom& geo = g->geo;
+  cudaStream_t s = g->stream;
+  const double* dinv = jac ? jac->inv_sqrt : nullptr;
+  const double2* tw = g->twiddle;
+  constexpr bool GJ = KIND == JFFTB_PC_GREEN_JACOBI;
+  constexpr int F = GJ ? 2 : 1;
+  fused_stage_A(geo, s, F, INIT ? FUSED_INIT : FUSED_ITER, B.st, B.rs, B.kp, dinv, B.spec, tw, bt);
+  fused_stage_B(geo, s, false, B.st, B.spec, F * geo.d, tw, bt);
+  const int scount = fused_stage_C(geo, s, F, false, B.st, gpc, gterm, B.spec, B.spart, tw, bt);
+  finalize_kernel<KIND, INIT><<<bt.L, 1024, 0, s>>>(B.st, B.spart, scount, 2, B.upart, kRedBlocks,
+                                                    B.hist, 2 * (int64_t)scount, B.hstride);
+  JF_LAUNCHED();
+  double2* z = B.spec + (GJ ? geo.d * fused_component_stride(geo) : 0);
+  fused_stage_B(geo, s, true, B.st, z, geo.d, tw, bt);
+  fused_stage_I(geo, s, INIT ? FUSED_INIT : FUSED_ITER, B.st, z, GJ ? dinv : nullptr, B.p, B.x, tw,
+                bt);
+}
+
+void pcg_dispatch_batch(int kind, bool init, jfftb_op* op, jfftb_jacobi* jac, jfftb_green* gpc,
+                        jfftb_green* gterm, const PcgBuffers& B, const Batch& bt) {
+  jfftb_grid* g = op->grid;
+  require(g->fused && (kind == JFFTB_PC_GREEN || kind == JFFTB_PC_GREEN_JACOBI),
+          "batched solves run the fused spectral kinds");
+  if (!init) {
+    launch_stencil_batch(g->geo, g->stream, B.p, op->rho, op->lambda0, op->mu0, B.kp, B.kpart, bt.L,
+                         bt.vs);
+    alpha_kernel<<<bt.L, 1024, 0, g->stream>>>(B.st, B.kpart, B.kcount, 1, B.kcount);
+    JF_LAUNCHED();
+  }
+  if (kind == JFFTB_PC_GREEN_JACOBI) {
+    init ? pcg_phase_batch<JFFTB_PC_GREEN_JACOBI, true>(g, jac, gpc, gterm, B, bt)
+         : pcg_phase_batch<JFFTB_PC_GREEN_JACOBI, false>(g, jac, gpc, gterm, B, bt);
+  } else {
+    init ? pcg_phase_batch<JFFTB_PC_GREEN, true>(g, jac, gpc, gterm, B, bt)
+         : pcg_phase_batch<JFFTB_PC_GREEN, false>(g, jac, gpc, gterm, B, bt);
+  }
+}
+
 void launch_alpha(cudaStream_t s, PcgState* st, const double* partials, int count, int stride) {
-  alpha_kernel<<<1, 1024, 0, s>>>(st, partials, count, stride);
+  alpha_kernel<<<1, 1024, 0, s>>>(st, partials, count, stride, 0);
   JF_LAUNCHED();
 }
 

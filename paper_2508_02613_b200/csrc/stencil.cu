@@ -120,7 +120,8 @@ template <int MODE, bool SCALE>
 __global__ void __launch_bounds__(BX3* BY3, MINB3)
     stencil3d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
               double lam0, double mu0, EbarT E, double* __restrict__ out,
-              double* __restrict__ partials, int chunk, int ext) {
+              double* __restrict__ partials, int chunk, int ext, int nchunks,
+              int64_t bstride) {
   constexpr bool HAS_U = MODE != VOX_RHS;
   extern __shared__ double smem[];
   double(*U)[3][BY3 + 1][BX3 + 1] = reinterpret_cast<double(*)[3][BY3 + 1][BX3 + 1]>(smem);
@@ -138,7 +139,12 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   auto in_row = [&](int y) { return ext ? min(y + 1, n1 + 1) : wrapi(y, n1); };
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int X0 = blockIdx.x * (BX3 - 1), Y0 = blockIdx.y * (BY3 - 1);
-  const int k0 = blockIdx.z * chunk;
+  // batched right-hand sides: blockIdx.z = rhs * nchunks + chunk; u and out
+  // are bstride doubles apart (rho is shared)
+  const int bl = (int)blockIdx.z / nchunks;
+  if (u) u += bl * bstride;
+  out += bl * bstride;
+  const int k0 = ((int)blockIdx.z % nchunks) * chunk;
   const int k1 = min(k0 + chunk, n0);
   const int gx = X0 - 1 + tx, gy = Y0 - 1 + ty;
   const int c2 = wrapi(gx, n2);
@@ -419,12 +425,14 @@ StencilLaunch stencil_config(const Geom& g) {
 template <int MODE, bool SCALE>
 void launch_mode(const Geom& g, cudaStream_t s, const StencilLaunch& L, const double* u,
                  const double* rho, double lam, double mu, const EbarT& E, double* out,
-                 double* partials, int ext) {
+                 double* partials, int ext, int nb = 1, int64_t bstride = 0) {
   if (g.d == 3) {
     static std::atomic<uint64_t> attr{0};  // per template instance and device
     set_smem_once(stencil3d<MODE, SCALE>, S3_BYTES, attr);
-    stencil3d<MODE, SCALE><<<L.grid, L.block, S3_BYTES, s>>>(g, u, rho, lam, mu, E, out,
-                                                             partials, L.chunk, ext);
+    dim3 grid = L.grid;
+    grid.z *= nb;
+    stencil3d<MODE, SCALE><<<grid, L.block, S3_BYTES, s>>>(g, u, rho, lam, mu, E, out, partials,
+                                                           L.chunk, ext, L.grid.z, bstride);
   }
   else
     stencil2d<MODE, SCALE><<<L.grid, L.block, 0, s>>>(g, u, rho, lam, mu, E, out, partials,
@@ -458,6 +466,26 @@ int launch_stencil(const Geom& g, cudaStream_t s, int mode, const double* u, con
     launch_mode<VOX_RHS, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr, ext);
   } else {
     launch_mode<VOX_RES, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr, ext);
+  }
+  return L.grid.x * L.grid.y * L.grid.z;
+}
+
+// K u for nb right-hand sides bstride doubles apart (3-D, one launch; the
+// partials of rhs b start at b * stencil_blocks(g))
+int launch_stencil_batch(const Geom& g, cudaStream_t s, const double* u, const double* rho,
+                         double lam, double mu, double* out, double* curv_partials, int nb,
+                         int64_t bstride) {
+  require(g.d == 3 || nb == 1, "batched stencil is 3-D");
+  if (nb == 1) return launch_stencil(g, s, ST_K, u, rho, lam, mu, nullptr, out, curv_partials);
+  StencilLaunch L = stencil_config(g);
+  const EbarT E = make_ebar(g.d, nullptr);
+  if (g.iso) {
+    const double sc = g.w * g.hinv[0] * g.hinv[0];
+    launch_mode<VOX_K, false>(g, s, L, u, rho, lam * sc, mu * sc, E, out, curv_partials, 0, nb,
+                              bstride);
+  } else {
+    launch_mode<VOX_K, true>(g, s, L, u, rho, lam * g.w, mu * g.w, E, out, curv_partials, 0, nb,
+                             bstride);
   }
   return L.grid.x * L.grid.y * L.grid.z;
 }

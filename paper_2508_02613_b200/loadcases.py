@@ -25,7 +25,8 @@ import numpy as np
 from . import _native as N
 from .grid import mandel_dim
 from .operators import grid_dim, op_handle
-from .solver import CONVERGED, DEFAULT_ETA_CG, DEFAULT_MAX_ITER, SolverAbortError, pcg_device
+from .solver import (CONVERGED, DEFAULT_ETA_CG, DEFAULT_MAX_ITER, SolverAbortError, pcg_device,
+                     pcg_device_batch)
 
 
 @dataclass
@@ -45,10 +46,12 @@ def _torch():
 
 def solve_load_cases(op, preconditioner, green, loads=None, eta: float = DEFAULT_ETA_CG,
                      max_iter: int = DEFAULT_MAX_ITER, keep_solutions: bool = False,
-                     cap_tolerance: float = 1e3) -> LoadCaseReport:
+                     cap_tolerance: float = 1e3, batch: bool = True) -> LoadCaseReport:
     """Solve K u_g = f(Ebar_g) for every load g (topopt.py:98-127).
 
     ``loads``: (L, M) Mandel strains, L <= 6 (default: the M unit loads).
+    ``batch``: run the L solves side by side (jfftb_pcg_batch) where the
+    grid and kind allow it; each solve keeps its own termination.
     Returns a :class:`LoadCaseReport`; with ``keep_solutions`` its
     ``solutions`` is the (L, d, n, ...) float64 CUDA tensor of the solves.
     """
@@ -66,17 +69,30 @@ def solve_load_cases(op, preconditioner, green, loads=None, eta: float = DEFAULT
     dev = torch.device("cuda", N.device_id())
     shape = (d,) + (op.grid.n,) * d
     us = torch.empty((L,) + shape, dtype=torch.float64, device=dev)
-    rhs = torch.empty(shape, dtype=torch.float64, device=dev)
-    torch.cuda.synchronize(dev)
     kind = preconditioner.kind
     green_pc = preconditioner.green.handle if preconditioner.green is not None else None
     jac = preconditioner.jacobi.handle if preconditioner.jacobi is not None else None
-    its, terms, hists = [], [], []
+    n = op.grid.n
+    # batched: every stage of the L solves in one launch (3-D power-of-two
+    # grids, spectral kinds); otherwise one solve after the other
+    batched = (batch and d == 3 and kind in ("green", "green-jacobi") and 16 <= n <= 2048
+               and n & (n - 1) == 0)
+    rhs = torch.empty(((L,) if batched else ()) + shape, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    results = []
     for g in range(L):
         e = np.ascontiguousarray(E[g])
-        N.check(lib.jfftb_assemble_rhs(h.ptr, N.dptr(e), C.c_void_p(rhs.data_ptr()), N.DEVICE))
-        it, hist, term, _ = pcg_device(h, kind, green.handle, jac, rhs.data_ptr(),
-                                       us[g].data_ptr(), eta, max_iter, green_pc_h=green_pc)
+        dst = rhs[g] if batched else rhs
+        N.check(lib.jfftb_assemble_rhs(h.ptr, N.dptr(e), C.c_void_p(dst.data_ptr()), N.DEVICE))
+        if not batched:
+            it, hist, term, _ = pcg_device(h, kind, green.handle, jac, rhs.data_ptr(),
+                                           us[g].data_ptr(), eta, max_iter, green_pc_h=green_pc)
+            results.append((it, hist, term))
+    if batched:
+        results, _ = pcg_device_batch(h, kind, green.handle, jac, L, rhs.data_ptr(),
+                                      us.data_ptr(), eta, max_iter, green_pc_h=green_pc)
+    its, terms, hists = [], [], []
+    for g, (it, hist, term) in enumerate(results):
         if term != CONVERGED and hist[-1] > cap_tolerance * eta:
             raise SolverAbortError(
                 f"load case {g}: iteration cap {max_iter} reached with squared Green norm "
@@ -115,6 +131,7 @@ def pairing_field(op, solutions, loads, weights):
 
 
 def _bench(n: int = 128, kind: str = "green-jacobi"):  # pragma: no cover
+    # python -m paper_2508_02613_b200.loadcases [n] [kind]
     """Six 3-D load cases on BASELINE config 3 (128^3 spheres): wall time of
     the device driver (assembly, solves, pairings) and its throughput."""
     import json
@@ -132,17 +149,23 @@ def _bench(n: int = 128, kind: str = "green-jacobi"):  # pragma: no cover
     op = make_operator(G.ScalarField(grid, rho), mat)
     green = assemble_green(grid, mat)
     pc = build_preconditioner(kind, op, green)
-    solve_load_cases(op, pc, green, loads=np.eye(6)[:1], max_iter=5, cap_tolerance=1e300)
-    _torch().cuda.synchronize()
-    t0 = time.perf_counter()
-    rep = solve_load_cases(op, pc, green)
-    dt = time.perf_counter() - t0
-    its = sum(rep.iterations)
-    print(json.dumps({"what": f"6 load cases, config 3 ({n}^3 spheres), {kind}, eta 1e-6",
-                      "seconds": dt, "iterations": rep.iterations,
-                      "GDOF_it_per_s": 3 * n ** 3 * its / dt / 1e9,
-                      "stress_diag": np.diag(rep.stress).tolist()}))
+    out = {"what": f"6 load cases, config 3 ({n}^3 spheres), {kind}, eta 1e-6"}
+    for batch in (True, False, True, False):
+        solve_load_cases(op, pc, green, loads=np.eye(6)[:2], max_iter=5, cap_tolerance=1e300,
+                         batch=batch)
+        _torch().cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = solve_load_cases(op, pc, green, batch=batch)
+        dt = time.perf_counter() - t0
+        its = sum(rep.iterations)
+        out["batched" if batch else "sequential"] = {
+            "seconds": dt, "iterations": rep.iterations,
+            "GDOF_it_per_s": 3 * n ** 3 * its / dt / 1e9,
+            "stress_diag": np.diag(rep.stress).tolist()}
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":  # pragma: no cover
-    _bench()
+    import sys
+    _bench(*([int(sys.argv[1])] if len(sys.argv) > 1 else []) +
+           ([sys.argv[2]] if len(sys.argv) > 2 else []))

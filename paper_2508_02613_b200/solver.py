@@ -91,6 +91,29 @@ def pcg_device(op_h: N.OpHandle, kind: str, green_h: N.GreenHandle, jac_h, rhs_p
         wall.value
 
 
+def pcg_device_batch(op_h: N.OpHandle, kind: str, green_h: N.GreenHandle, jac_h, nrhs: int,
+                     rhs_ptr: int, x_ptr: int, eta: float, max_iter: int, green_pc_h=None):
+    """``nrhs`` device-resident solves at once (jfftb_pcg_batch: one launch
+    per stage for all of them; fused 3-D grids, green / green-jacobi).
+    ``rhs_ptr``/``x_ptr``: nrhs vector fields back to back on the device.
+    Returns per solve (iterations, history, terminated) and the wall time."""
+    m = int(max_iter) + 1
+    hist = np.zeros(nrhs * m)
+    iters = (C.c_int * nrhs)()
+    terms = (C.c_int * nrhs)()
+    wall = C.c_double(0.0)
+    gpc = (green_pc_h or green_h).ptr
+    jac = jac_h.ptr if (jac_h is not None and kind == "green-jacobi") else None
+    status = N.load().jfftb_pcg_batch(op_h.ptr, N.KIND_CODES[kind], gpc, jac, green_h.ptr, nrhs,
+                                      C.c_void_p(rhs_ptr), N.DEVICE, float(eta), int(max_iter),
+                                      C.c_void_p(x_ptr), N.dptr(hist), iters, terms,
+                                      C.byref(wall))
+    N.check(status)
+    out = [(iters[l], hist[l * m:l * m + iters[l] + 1].tolist(),
+            CONVERGED if terms[l] == 0 else ITERATION_CAP) for l in range(nrhs)]
+    return out, wall.value
+
+
 def _dot(a, b) -> float:
     return float(np.vdot(a.values, b.values))
 

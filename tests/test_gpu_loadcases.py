@@ -89,3 +89,25 @@ def test_cap_policy_and_validation():
         solve_load_cases(op, pc, green, loads=np.ones((7, 3)))
     with pytest.raises(ValueError):
         solve_load_cases(op, pc, green, loads=np.ones((2, 6)))
+
+
+@pytest.mark.parametrize("kind", ["green-jacobi", "green"])
+def test_batched_matches_sequential(kind):
+    """jfftb_pcg_batch (one launch per stage for all load cases) against the
+    same solves one after the other: same iteration counts, histories and
+    solutions to round-off (the batched pass C reduces over a different
+    number of blocks), same stress matrix."""
+    rho, lam, mu, lengths, grid, mat, op = _problem(3, 32, 3)
+    green = assemble_green(grid, mat)
+    pc = build_preconditioner(kind, op, green)
+    loads = np.eye(6)[[0, 2, 5]]
+    a = solve_load_cases(op, pc, green, loads=loads, keep_solutions=True, batch=True)
+    b = solve_load_cases(op, pc, green, loads=loads, keep_solutions=True, batch=False)
+    for g in range(3):
+        assert abs(a.iterations[g] - b.iterations[g]) <= 1
+        k = min(len(a.residual_history[g]), len(b.residual_history[g]), 10)
+        ha, hb = np.array(a.residual_history[g][:k]), np.array(b.residual_history[g][:k])
+        assert np.abs(ha - hb).max() <= 1e-12 * hb[0]
+    assert np.abs(a.stress - b.stress).max() <= 1e-9 * np.abs(b.stress).max()
+    ua, ub = a.solutions.cpu().numpy(), b.solutions.cpu().numpy()
+    assert np.abs(ua - ub).max() <= 1e-7 * np.abs(ub).max()
