@@ -132,6 +132,10 @@ struct jfftb_grid {
   jfftb::PcgState* wsb_host = nullptr;
   int wsb_L = 0;
   jfftb::PcgState* ws_host = nullptr;  // pinned mirror of the device state
+  // pass I / stencil overlap (pcg.cu tail_I_KA): a higher-priority side
+  // stream and fork / join events, created on first use
+  cudaStream_t side_stream = nullptr;
+  std::vector<cudaEvent_t> ovl_ev;
   // stage profile (jfftb_profile_*)
   bool prof = false;
   std::vector<cudaEvent_t> ev_free;
@@ -318,6 +322,15 @@ int launch_stencil(const Geom& g, cudaStream_t s, int mode, const double* u,
                    const double* rho, double lam, double mu, const double* ebar_mandel,
                    double* out, double* curv_partials, int ext = 0);
 int stencil_blocks(const Geom& g);
+// 3-D tile rows of the stencil launch and output rows per tile row
+int stencil_tile_rows(const Geom& g);
+int stencil_tile_height(const Geom& g);
+struct PcgState;
+// K p on tile rows [ty0, ty1) (3-D), predicated on st->done; partial b keeps
+// its full-launch index
+void launch_stencil_rows(const Geom& g, cudaStream_t s, const double* u, const double* rho,
+                         double lam, double mu, double* out, double* curv_partials,
+                         const PcgState* st, int ty0, int ty1);
 // K u for nb right-hand sides bstride doubles apart (one launch; returns the
 // partials per right-hand side, rhs b's at curv_partials + b * that)
 int launch_stencil_batch(const Geom& g, cudaStream_t s, const double* u, const double* rho,
@@ -452,6 +465,10 @@ int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const 
 void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                    const double2* zspec, const double* dinv, double* p, double* x,
                    const double2* tw, const Batch& bt);
+// pass I restricted to axis-1 rows [row0, row1) (3-D)
+void fused_stage_I_rows(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
+                        const double2* zspec, const double* dinv, double* p, double* x,
+                        const double2* tw, int row0, int row1);
 int64_t fused_component_stride(const Geom& geo);
 // distributed solves (dist.cu): one rank's k0-slab of the spectral passes
 struct SpecSlab {

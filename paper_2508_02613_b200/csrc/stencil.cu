@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
     stencil3d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
               double lam0, double mu0, EbarT E, double* __restrict__ out,
               double* __restrict__ partials, int chunk, int ext, int nchunks,
-              int64_t bstride) {
+              int64_t bstride, const PcgState* __restrict__ st, int yoff, int ytot) {
   constexpr bool HAS_U = MODE != VOX_RHS;
   extern __shared__ double smem[];
   double(*U)[3][BY3 + 1][BX3 + 1] = reinterpret_cast<double(*)[3][BY3 + 1][BX3 + 1]>(smem);
@@ -137,8 +137,12 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   // axis 1); out keeps the n1 rows
   const int64_t Pin = ext ? P + 2 * (int64_t)n2 : P, Nin = (int64_t)n0 * Pin;
   auto in_row = [&](int y) { return ext ? min(y + 1, n1 + 1) : wrapi(y, n1); };
+  // PCG direction update predicated on the solve state (no work once done);
+  // tile rows [yoff, yoff + gridDim.y) of ytot (a row group, pcg.cu)
+  if (st && st->done) return;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int X0 = blockIdx.x * (BX3 - 1), Y0 = blockIdx.y * (BY3 - 1);
+  const int by = blockIdx.y + yoff;
+  const int X0 = blockIdx.x * (BX3 - 1), Y0 = by * (BY3 - 1);
   // batched right-hand sides: blockIdx.z = rhs * nchunks + chunk; u and out
   // are bstride doubles apart (rho is shared)
   const int bl = (int)blockIdx.z / nchunks;
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
   if (MODE == VOX_K && partials) {
     const double s = block_sum(csum, red);
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      partials[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s;
+      partials[blockIdx.x + gridDim.x * (by + ytot * blockIdx.z)] = s;
   }
 }
 
@@ -425,14 +429,18 @@ StencilLaunch stencil_config(const Geom& g) {
 template <int MODE, bool SCALE>
 void launch_mode(const Geom& g, cudaStream_t s, const StencilLaunch& L, const double* u,
                  const double* rho, double lam, double mu, const EbarT& E, double* out,
-                 double* partials, int ext, int nb = 1, int64_t bstride = 0) {
+                 double* partials, int ext, int nb = 1, int64_t bstride = 0,
+                 const PcgState* st = nullptr, int ty0 = 0, int ty1 = -1) {
   if (g.d == 3) {
     static std::atomic<uint64_t> attr{0};  // per template instance and device
     set_smem_once(stencil3d<MODE, SCALE>, S3_BYTES, attr);
     dim3 grid = L.grid;
     grid.z *= nb;
+    if (ty1 < 0) ty1 = (int)L.grid.y;
+    grid.y = ty1 - ty0;
     stencil3d<MODE, SCALE><<<grid, L.block, S3_BYTES, s>>>(g, u, rho, lam, mu, E, out, partials,
-                                                           L.chunk, ext, L.grid.z, bstride);
+                                                           L.chunk, ext, L.grid.z, bstride, st,
+                                                           ty0, (int)L.grid.y);
   }
   else
     stencil2d<MODE, SCALE><<<L.grid, L.block, 0, s>>>(g, u, rho, lam, mu, E, out, partials,
@@ -468,6 +476,27 @@ int launch_stencil(const Geom& g, cudaStream_t s, int mode, const double* u, con
     launch_mode<VOX_RES, true>(g, s, L, u, rho, -lam * g.w, -mu * g.w, E, out, nullptr, ext);
   }
   return L.grid.x * L.grid.y * L.grid.z;
+}
+
+int stencil_tile_rows(const Geom& g) { return g.d == 3 ? (int)stencil_config(g).grid.y : 1; }
+int stencil_tile_height(const Geom& g) { return g.d == 3 ? BY3 - 1 : 0; }
+
+// K p on the 3-D tile rows [ty0, ty1) (output rows [ty0, ty1) x (BY3 - 1)),
+// predicated on the PCG state; partials land at the full launch's indices
+void launch_stencil_rows(const Geom& g, cudaStream_t s, const double* u, const double* rho,
+                         double lam, double mu, double* out, double* curv_partials,
+                         const PcgState* st, int ty0, int ty1) {
+  require(g.d == 3, "row-group stencil is 3-D");
+  StencilLaunch L = stencil_config(g);
+  const EbarT E = make_ebar(3, nullptr);
+  if (g.iso) {
+    const double sc = g.w * g.hinv[0] * g.hinv[0];
+    launch_mode<VOX_K, false>(g, s, L, u, rho, lam * sc, mu * sc, E, out, curv_partials, 0, 1, 0,
+                              st, ty0, ty1);
+  } else {
+    launch_mode<VOX_K, true>(g, s, L, u, rho, lam * g.w, mu * g.w, E, out, curv_partials, 0, 1, 0,
+                             st, ty0, ty1);
+  }
 }
 
 // K u for nb right-hand sides bstride doubles apart (3-D, one launch; the
