@@ -326,10 +326,7 @@ void run_iteration_graph(jfftb_grid* g, int kind, jfftb_op* op, jfftb_jacobi* ja
     JF_CUDA(ec);
     g->iter_launches = (int)(g_launches - before);
     g_launches = before;
-    // node priorities: the stencil row groups of the pass-I overlap run on a
-    // higher-priority stream (pcg.cu tail_I_KA)
-    const cudaError_t e =
-        cudaGraphInstantiate(&g->iter_graph, graph, cudaGraphInstantiateFlagUseNodePriority);
+    const cudaError_t e = cudaGraphInstantiate(&g->iter_graph, graph, 0);
     cudaGraphDestroy(graph);
     JF_CUDA(e);
     for (int i = 0; i < kIterKey; ++i) g->iter_key[i] = key[i];
@@ -527,8 +524,6 @@ void grid_free(jfftb_grid* g) {
     if (g->twiddle) cudaFree(g->twiddle);
     free_host_staging(g);
     drop_iteration_graph(g);
-    for (auto e : g->ovl_ev) cudaEventDestroy(e);
-    if (g->side_stream) cudaStreamDestroy(g->side_stream);
     prof_collect(g, 0, true);
     for (auto e : g->ev_free) cudaEventDestroy(e);
     cudaStreamDestroy(g->own_stream);

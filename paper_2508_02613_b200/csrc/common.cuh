@@ -132,10 +132,6 @@ struct jfftb_grid {
   jfftb::PcgState* wsb_host = nullptr;
   int wsb_L = 0;
   jfftb::PcgState* ws_host = nullptr;  // pinned mirror of the device state
-  // pass I / stencil overlap (pcg.cu tail_I_KA): a higher-priority side
-  // stream and fork / join events, created on first use
-  cudaStream_t side_stream = nullptr;
-  std::vector<cudaEvent_t> ovl_ev;
   // stage profile (jfftb_profile_*)
   bool prof = false;
   std::vector<cudaEvent_t> ev_free;
@@ -465,10 +461,7 @@ int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const 
 void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                    const double2* zspec, const double* dinv, double* p, double* x,
                    const double2* tw, const Batch& bt);
-// pass I restricted to axis-1 rows [row0, row1) (3-D)
-void fused_stage_I_rows(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
-                        const double2* zspec, const double* dinv, double* p, double* x,
-                        const double2* tw, int row0, int row1);
+
 int64_t fused_component_stride(const Geom& geo);
 // distributed solves (dist.cu): one rank's k0-slab of the spectral passes
 struct SpecSlab {

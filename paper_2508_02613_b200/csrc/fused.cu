@@ -74,7 +74,6 @@ struct FGeom {
   // state each; vector fields vs doubles and spectra bss complex apart
   int L;
   int64_t vs, bss;
-  int64_t toff;    // pass I: first column tile of a row-group launch
   __device__ __forceinline__ int64_t row_off(int64_t row) const {
     const int64_t k = row >> rsh;
     const int k1 = (int)(row & ((1 << rsh) - 1));
@@ -714,7 +713,7 @@ __global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
   if (x) x += bl * g.vs;
   if (MODE == FM_ITER && !st->xupd) return;
   if (MODE == FM_INIT && st->done) return;
-  const int64_t col0 = ((int64_t)blockIdx.x + g.toff) * TW;
+  const int64_t col0 = (int64_t)blockIdx.x * TW;
   const double2* zc = zspec + c * g.CS + col0;
   for (int e = threadIdx.x; e < (M + 1) * TW; e += NT) {
     const int k = e / TW, col = e % TW;
@@ -806,7 +805,6 @@ FGeom fgeom(const Geom& g) {
   f.L = 1;
   f.vs = 0;
   f.bss = 0;
-  f.toff = -1;  // all column tiles
   return f;
 }
 
@@ -928,12 +926,8 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
   auto k = passI<M, MODE>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  // g.toff / tiles: a row group of the column tiles (pcg.cu), else all
-  const int64_t tiles = g.toff < 0 ? g.PS / TW : g.toff >> 32;
-  FGeom gg = g;
-  gg.toff = g.toff < 0 ? 0 : (g.toff & 0xffffffff);
-  dim3 grid((unsigned)tiles, g.d * g.L);
-  k<<<grid, NT, smem, s>>>(gg, st, zspec, dinv, p, x, out, tw);
+  dim3 grid((unsigned)(g.PS / TW), g.d * g.L);
+  k<<<grid, NT, smem, s>>>(g, st, zspec, dinv, p, x, out, tw);
   JF_LAUNCHED();
 }
 
@@ -1113,18 +1107,6 @@ void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st
                    const double2* zspec, const double* dinv, double* p, double* x,
                    const double2* tw, const Batch& bt) {
   launchI(fgeom_b(geo, bt), s, mode, st, zspec, dinv, p, x, nullptr, tw);
-}
-// pass I on the column tiles of axis-1 rows [row0, row1) (the tiles are
-// tw_a(n0/2) columns wide along the contiguous axis)
-void fused_stage_I_rows(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
-                        const double2* zspec, const double* dinv, double* p, double* x,
-                        const double2* tw, int row0, int row1) {
-  FGeom g = fgeom(geo);
-  const int TW = tw_a(g.M0);
-  const int64_t per_row = g.nlast / TW;  // column tiles per axis-1 row (3-D)
-  const int64_t t0 = row0 * per_row, nt = (int64_t)(row1 - row0) * per_row;
-  g.toff = (nt << 32) | t0;
-  launchI(g, s, mode, st, zspec, dinv, p, x, nullptr, tw);
 }
 int64_t fused_component_stride(const Geom& geo) { return fgeom(geo).CS; }
 

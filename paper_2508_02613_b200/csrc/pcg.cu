@@ -221,69 +221,21 @@ static void pcg_precond_phase(jfftb_grid* g, jfftb_jacobi* jac, jfftb_green* gpc
   }
 }
 
-// JFFTB_OVERLAP=0: the stencil runs after pass I instead of overlapping it
-static bool overlap_enabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("JFFTB_OVERLAP");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
 // The end of an iteration (3-D fused spectral kinds): pass I writes the new
-// direction p_{k+1} (and x) in G groups of axis-1 rows on the grid's stream,
-// and the stencil K p_{k+1} of the NEXT iteration starts on a higher-priority
-// side stream as soon as the row groups it reads are written (one halo row on
-// each side), so the fp64-issue-bound stencil runs alongside the
-// HBM-bound pass I instead of after it.  The side stream joins back before
-// alpha.  Without overlap (profiling, small grids, JFFTB_OVERLAP=0) the two
-// run back to back.  Every kernel is predicated on the PCG state.
+// direction p_{k+1} (and x), then the NEXT iteration's stencil K p_{k+1} runs
+// right away, predicated on the PCG state like every other pass, so the
+// iterations queued past convergence cost nothing.  (Running the stencil in
+// row groups on a side stream alongside pass I was measured: no gain at
+// 512^3 -- 18.30 vs 18.14 ms per iteration -- the two do not co-reside on an
+// SM and the board is power-capped.)
 static void tail_I_KA(jfftb_op* op, jfftb_grid* g, int mode, const PcgBuffers& B,
                       const double2* z, const double* dinv) {
   const Geom& geo = g->geo;
   cudaStream_t s = g->stream;
-  const int TR = stencil_tile_rows(geo), TH = stencil_tile_height(geo);
-  const int G = geo.d == 3 ? std::min(8, TR / 2) : 0;
-  if (geo.d != 3 || G < 3 || g->prof || !overlap_enabled()) {
-    fused_stage_I(geo, s, mode, B.st, z, dinv, B.p, B.x, g->twiddle, Batch{});
-    if (!g->prof) {
-      launch_stencil_rows(geo, s, B.p, op->rho, op->lambda0, op->mu0, B.kp, B.kpart, B.st, 0, TR);
-    }
-    return;
-  }
-  if (!g->side_stream) {
-    int lo = 0, hi = 0;
-    JF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    JF_CUDA(cudaStreamCreateWithPriority(&g->side_stream, cudaStreamNonBlocking, hi));
-  }
-  while ((int)g->ovl_ev.size() < G + 1) {
-    cudaEvent_t e;
-    JF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    g->ovl_ev.push_back(e);
-  }
-  std::vector<int> a(G + 1), R(G + 1);
-  for (int h = 0; h <= G; ++h) {
-    a[h] = h * TR / G;
-    R[h] = std::min(a[h] * TH, geo.n[1]);
-  }
-  for (int h = 0; h < G; ++h) {
-    fused_stage_I_rows(geo, s, mode, B.st, z, dinv, B.p, B.x, g->twiddle, R[h], R[h + 1]);
-    JF_CUDA(cudaEventRecord(g->ovl_ev[h], s));
-  }
-  cudaStream_t side = g->side_stream;
-  auto ka = [&](int h) {
-    launch_stencil_rows(geo, side, B.p, op->rho, op->lambda0, op->mu0, B.kp, B.kpart, B.st, a[h],
-                        a[h + 1]);
-  };
-  // group h reads p rows [R[h] - 1, R[h + 1]]: row groups h - 1 .. h + 1
-  for (int h = 1; h <= G - 2; ++h) {
-    JF_CUDA(cudaStreamWaitEvent(side, g->ovl_ev[h + 1], 0));
-    ka(h);
-  }
-  ka(G - 1);  // wraps to row group 0; rows of G - 1 waited above
-  ka(0);      // reads the last row of group G - 1
-  JF_CUDA(cudaEventRecord(g->ovl_ev[G], side));
-  JF_CUDA(cudaStreamWaitEvent(s, g->ovl_ev[G], 0));
+  fused_stage_I(geo, s, mode, B.st, z, dinv, B.p, B.x, g->twiddle, Batch{});
+  if (!g->prof)
+    launch_stencil_rows(geo, s, B.p, op->rho, op->lambda0, op->mu0, B.kp, B.kpart, B.st, 0,
+                        stencil_tile_rows(geo));
 }
 
 // Fused-spectral variant (power-of-two grids): green / green-jacobi run the
@@ -332,7 +284,7 @@ static void pcg_precond_phase_fused(jfftb_op* op, jfftb_grid* g, jfftb_jacobi* j
     fused_stage_B(geo, s, true, B.st, z, geo.d, tw, Batch{});
     if (!INIT) prof_mark(g);
     if (g->geo.d == 3) {
-      // pass I and the next iteration's stencil, overlapped
+      // pass I, then the next iteration's stencil
       tail_I_KA(op, g, INIT ? FUSED_INIT : FUSED_ITER, B, z, GJ ? dinv : nullptr);
     } else {
       fused_stage_I(geo, s, INIT ? FUSED_INIT : FUSED_ITER, B.st, z, GJ ? dinv : nullptr, B.p,
@@ -351,7 +303,7 @@ static void pcg_precond_phase_fused(jfftb_op* op, jfftb_grid* g, jfftb_jacobi* j
 }
 
 // the fused 3-D spectral kinds compute K p at the end of the previous
-// iteration (tail_I_KA, overlapped with pass I)
+// iteration (tail_I_KA)
 template <int KIND>
 static constexpr bool ka_in_tail() {
   return KIND == JFFTB_PC_GREEN || KIND == JFFTB_PC_GREEN_JACOBI;
