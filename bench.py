@@ -147,7 +147,34 @@ def _ref_worker_solve(iters):
 
 
 def cpu_sample_n(d):
-    return 64 if d == 3 else 256
+    """the CPU baseline runs the oracle at 128^3 (BASELINE config
+    3's size) on a sample of the workload generator; 2-D at 1024^2."""
+    return 128 if d == 3 else 1024
+
+
+def host_info():
+    """CPU model, core count, NumPy / BLAS versions and the BLAS thread
+    setting of the host the CPU arm runs on."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = "unknown"
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name', '?')} {b.get('version', '?')}"
+    except Exception:
+        pass
+    mem = os.sysconf("SC_PHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    return {"cpu_model": model, "nproc": os.cpu_count(), "host_mem_gb": round(mem / 2 ** 30, 1),
+            "numpy": np.__version__, "blas": blas,
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS", "unset")}
 
 
 def run_reference(args, rank):
@@ -156,8 +183,13 @@ def run_reference(args, rank):
     import multiprocessing as mp
     d, nfull, _, _ = WORKLOADS[args.workload]
     n = cpu_sample_n(d)
-    cores = os.cpu_count() or 1
-    iters = 5
+    info = host_info()
+    # one single-threaded oracle solve per core, as many as host memory holds
+    # (a 128^3 oracle solve peaks at ~4 GB)
+    per_proc_gb = 4.5 if d == 3 else 1.0
+    cores = max(1, min(os.cpu_count() or 1, int(info["host_mem_gb"] * 0.8 // per_proc_gb)))
+    iters = 2
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"  # NumPy's kernels here are single-threaded anyway
     ctx = mp.get_context("fork")
     with ctx.Pool(cores, initializer=_ref_worker_init, initargs=(d, n, args.kind, 0)) as pool:
         for _ in range(max(args.warmup, 0)):
@@ -168,8 +200,9 @@ def run_reference(args, rank):
         dt = time.perf_counter() - t0
     dof_it = d * n ** d * iters * cores * args.steps
     value = dof_it / dt / 1e9
-    sample = (f"{cores} concurrent oracle PCG solves ({args.kind}) of {n}^{d} per step, "
-              f"{iters} iterations each (full {nfull}^{d} does not fit a NumPy oracle)")
+    sample = (f"{cores} concurrent single-threaded oracle PCG solves ({args.kind}) of the "
+              f"{n}^{d} sample per step, {iters} iterations each (the {nfull}^{d} cell needs "
+              f"~60 GB and ~150 s per iteration in the NumPy oracle)")
     line = {
         "impl": "reference", "metric": metric_name(args), "value": value, "unit": "GDOF-it/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -177,7 +210,7 @@ def run_reference(args, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_of(args),
         "cpu_baseline": {"value": value, "unit": "GDOF-it/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "host": info},
         "e2e": {"value": value, "unit": "GDOF-it/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -190,12 +223,14 @@ def cpu_baseline_single(args):
     n = cpu_sample_n(d)
     _ref_worker_init(d, n, args.kind, 0)
     _ref_worker_solve(1)
-    iters = 4
+    iters = 3
     t = _ref_worker_solve(iters)
     return {"value": d * n ** d * iters / t / 1e9, "unit": "GDOF-it/s", "cores": 1,
             "kind": "port",
             "sample": f"oracle PCG ({args.kind}) on a {n}^{d} sample of the workload "
-                      f"generator, {iters} iterations, {t:.1f} s, numpy single-threaded"}
+                      f"generator, {iters} iterations, {t:.1f} s, numpy single-threaded "
+                      "(1 core used)",
+            "host": host_info()}
 
 
 def metric_name(args):
@@ -330,9 +365,11 @@ def run_ours(args, rank, world):
                "model": "fused minimum (18d+1)U / (14d+1)U, SURVEY 8(d)"}
 
     # ---- e2e through the public API with host (pinned) buffers -----------
-    e2e = None
+    e2e = e2e_pg = None
     if args.e2e_steps > 0:
         e2e = run_e2e(args, P, torch, world)
+        # the reference hands over plain (pageable) NumPy arrays
+        e2e_pg = run_e2e(args, P, torch, world, pageable=True)
 
     line = {
         "metric": metric_name(args), "value": value, "unit": "GDOF-it/s", "n_gpus": world,
@@ -342,7 +379,7 @@ def run_ours(args, rank, world):
         "data": "synthetic (seeded, BASELINE.json config generator; see DESIGN.md)",
         "config": config_of(args), "roofline": roof, "roofline_iteration": roof_it,
         "stages_ms_per_iteration": {k: round(v["ms"], 4) for k, v in stages.items()},
-        "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "e2e": e2e, "e2e_pageable": e2e_pg, "gpu_launches": int(launches), "clocks": clk,
     }
     return line
 
@@ -448,7 +485,7 @@ def run_dist(args, rank, world):
     }
 
 
-def run_e2e(args, P, torch, world):
+def run_e2e(args, P, torch, world, pageable=False):
     from paper_2508_02613_b200 import grid as G
     from paper_2508_02613_b200.material import isotropic_material
     from paper_2508_02613_b200.operators import make_operator, op_handle
@@ -458,16 +495,21 @@ def run_e2e(args, P, torch, world):
     grid = G.make_grid(n, (1.0,) * d)
     mat = isotropic_material(P["lam"], P["mu"], d)
     # density and rhs live in pinned host memory (the caller's buffers)
-    rho_h = torch.empty(P["rho"].shape, dtype=torch.float64, pin_memory=True)
+    rho_h = torch.empty(P["rho"].shape, dtype=torch.float64, pin_memory=not pageable)
     rho_h.copy_(P["rho"])
-    rhs_h = torch.empty(P["rhs"].shape, dtype=torch.float64, pin_memory=True)
+    rhs_h = torch.empty(P["rhs"].shape, dtype=torch.float64, pin_memory=not pageable)
     rhs_h.copy_(P["rhs"])
-    op = make_operator(G.ScalarField(grid, rho_h.numpy()), mat)
+    if pageable:  # plain NumPy arrays, as the reference's callers hold them
+        rho_h, rhs_h = rho_h.numpy().copy(), rhs_h.numpy().copy()
+        rho_np, rhs_np = rho_h, rhs_h
+    else:
+        rho_np, rhs_np = rho_h.numpy(), rhs_h.numpy()
+    op = make_operator(G.ScalarField(grid, rho_np), mat)
     op_handle(op)  # operator assembly (density upload) is setup, as in the reference
     green = GreenOperator(grid, mat, P["green"])
     jac = JacobiDiagonal(grid, P["jac"]) if P["jac"] is not None else None
     pre = Preconditioner(args.kind, green=green, jacobi=jac)
-    rhs = G.VectorField(grid, rhs_h.numpy())
+    rhs = G.VectorField(grid, rhs_np)
     pcg(op, rhs, pre, green, eta=-1.0, max_iter=args.iters)  # warm
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -480,7 +522,8 @@ def run_e2e(args, P, torch, world):
     return {"value": value, "unit": "GDOF-it/s", "h2d_bytes_per_step": nbytes,
             "d2h_bytes_per_step": nbytes + 8 * (args.iters + 1),
             "api": "paper_2508_02613_b200.pcg(op, rhs, preconditioner, green) host VectorField "
-                   "(pinned), solution returned on the host"}
+                   f"({'pageable NumPy' if pageable else 'pinned'}), solution returned on the "
+                   "host (a fresh NumPy array)"}
 
 
 def _json_stdout():

@@ -135,7 +135,11 @@ def run(case: str) -> None:
     sl = (slice(None),) + (slice(None, None, s),) * d
     out = {"rho_sum": rho.sum(), "rho_min": rho.min(), "rho_max": rho.max(),
            "eps_bar": eb, "lam": lam, "mu": mu, "sample": s}
-    kinds = ("green-jacobi",) if big else ("green", "green-jacobi")
+    kinds = ("green-jacobi",) if big else (("green-jacobi", "green") if case.startswith("c5")
+                                           else ("green", "green-jacobi"))
+    # config 5 (contrast 1e6): Green converges to the tight tolerance only
+    # after thousands of iterations -- its tight solve is skipped
+    skip_tight = {"green"} if case.startswith("c5") else set()
     for kind in kinds:
         t = time.perf_counter()
         cap = 10 if big else FIXED[d]
@@ -159,6 +163,8 @@ def run(case: str) -> None:
         out[f"{kind}_std_terminated"] = term
         out[f"{kind}_std_hist"] = hist
         print(f"  {kind} eta=1e-6: {it} {term} ({time.perf_counter() - t:.0f}s)", flush=True)
+        if kind in skip_tight:
+            continue
         t = time.perf_counter()
         eta = TIGHT * hist[0]
         it, hist, term, x, sig = solver.solve(kind, eta, 5000)
