@@ -156,6 +156,9 @@ int jfftb_apply_green(jfftb_green* green, const double* r, double* out, int wher
  * EINVAL for odd n or a negative / non-finite probed diagonal. */
 int jfftb_jacobi_create(jfftb_op* op, jfftb_jacobi** out);
 int jfftb_jacobi_destroy(jfftb_jacobi* jac);
+/* JacobiDiagonal(grid, inv_sqrt) built by the caller (preconditioners.py:38-47
+ * is a plain container; the reference's tests construct it directly) */
+int jfftb_jacobi_from_array(jfftb_grid* g, const double* inv_sqrt, int where, jfftb_jacobi** out);
 /* JacobiDiagonal.inv_sqrt (vector field layout) */
 int jfftb_jacobi_export(jfftb_jacobi* jac, double* out, int where);
 

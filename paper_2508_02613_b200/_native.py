@@ -60,6 +60,7 @@ _SIGS = {
     "jfftb_apply_green": (C.c_int, [_P, _P, _P, C.c_int]),
     "jfftb_jacobi_create": (C.c_int, [_P, C.POINTER(_P)]),
     "jfftb_jacobi_destroy": (C.c_int, [_P]),
+    "jfftb_jacobi_from_array": (C.c_int, [_P, _P, C.c_int, C.POINTER(_P)]),
     "jfftb_jacobi_export": (C.c_int, [_P, _P, C.c_int]),
     "jfftb_apply_precond": (C.c_int, [C.c_int, _P, _P, _P, _P, C.c_int]),
     "jfftb_pcg": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, C.c_double, C.c_int, _P,
@@ -222,12 +223,18 @@ class GreenHandle(_Handle):
 class JacobiHandle(_Handle):
     _destroy = "jfftb_jacobi_destroy"
 
-    def __init__(self, op: OpHandle):
+    def __init__(self, op: OpHandle | None, grid: GridHandle | None = None, inv_sqrt=None):
+        """Probed from ``op`` (assemble_jacobi), or, with ``op=None``, uploaded
+        from a caller's ``inv_sqrt`` array on ``grid``."""
         out = C.c_void_p()
-        check(load().jfftb_jacobi_create(op.ptr, C.byref(out)))
+        if op is not None:
+            check(load().jfftb_jacobi_create(op.ptr, C.byref(out)))
+        else:
+            arr = np.ascontiguousarray(inv_sqrt, dtype=np.float64)
+            check(load().jfftb_jacobi_from_array(grid.ptr, vptr(arr), HOST, C.byref(out)))
         super().__init__(out)
         self.op = op
-        self.grid = op.grid
+        self.grid = op.grid if op is not None else grid
 
 
 _grid_cache: dict = {}

@@ -904,6 +904,27 @@ int jfftb_jacobi_create(jfftb_op* op, jfftb_jacobi** out) {
     auto* j = new jfftb_jacobi();
     op->refs.fetch_add(1);
     j->op = op;
+    j->grid = g;
+    j->inv_sqrt = diag;
+    *out = j;
+  });
+}
+
+int jfftb_jacobi_from_array(jfftb_grid* g, const double* inv_sqrt, int where, jfftb_jacobi** out) {
+  return guarded([&] {
+    require(g != nullptr && inv_sqrt != nullptr && out != nullptr, "null argument");
+    DeviceGuard dg(g->device);
+    const int64_t n = g->geo.d * g->geo.N;
+    DevBuf tin;
+    const double* src = stage_in(g, inv_sqrt, n, where, tin);
+    double* diag = nullptr;
+    JF_CUDA(cudaMalloc(&diag, sizeof(double) * n));
+    JF_CUDA(cudaMemcpyAsync(diag, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, g->stream));
+    JF_CUDA(cudaStreamSynchronize(g->stream));
+    auto* j = new jfftb_jacobi();
+    g->refs.fetch_add(1);
+    j->op = nullptr;
+    j->grid = g;
     j->inv_sqrt = diag;
     *out = j;
   });
@@ -913,21 +934,23 @@ int jfftb_jacobi_destroy(jfftb_jacobi* jac) {
   return guarded([&] {
     if (!jac) return;
     jfftb_op* op = jac->op;
+    jfftb_grid* g = jac->grid;
     {
-      DeviceGuard dg(op->grid->device);
-      cudaStreamSynchronize(op->grid->stream);
-      drop_iteration_graph(op->grid);  // it bakes in D^-1/2
+      DeviceGuard dg(g->device);
+      cudaStreamSynchronize(g->stream);
+      drop_iteration_graph(g);  // it bakes in D^-1/2
       cudaFree(jac->inv_sqrt);
     }
     delete jac;
-    op_release(op);
+    if (op) op_release(op);
+    else grid_release(g);
   });
 }
 
 int jfftb_jacobi_export(jfftb_jacobi* jac, double* out, int where) {
   return guarded([&] {
     require(jac != nullptr, "null jacobi");
-    jfftb_grid* g = jac->op->grid;
+    jfftb_grid* g = jac->grid;
     DeviceGuard dg(g->device);
     const int64_t n = g->geo.d * g->geo.N;
     require(out != nullptr, "null output");
@@ -944,9 +967,9 @@ int jfftb_jacobi_export(jfftb_jacobi* jac, double* out, int where) {
 int jfftb_apply_precond(int kind, jfftb_green* green, jfftb_jacobi* jac, const double* r,
                         double* out, int where) {
   return guarded([&] {
-    jfftb_grid* g = green ? green->grid : (jac ? jac->op->grid : nullptr);
+    jfftb_grid* g = green ? green->grid : (jac ? jac->grid : nullptr);
     require(g != nullptr, "preconditioner needs a Green operator or a Jacobi diagonal");
-    if (green && jac) require(green->grid == jac->op->grid, "grid mismatch");
+    if (green && jac) require(green->grid == jac->grid, "grid mismatch");
     DeviceGuard dg(g->device);
     const int64_t n = g->geo.d * g->geo.N;
     DevBuf tin, tout;
@@ -972,7 +995,7 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     if (kind == JFFTB_PC_GREEN || kind == JFFTB_PC_GREEN_JACOBI)
       require(green_pc != nullptr && green_pc->grid == g, "kind needs an assembled Green operator");
     if (kind == JFFTB_PC_JACOBI || kind == JFFTB_PC_GREEN_JACOBI)
-      require(jac != nullptr && jac->op->grid == g, "kind needs an assembled Jacobi diagonal");
+      require(jac != nullptr && jac->grid == g, "kind needs an assembled Jacobi diagonal");
     if (!green_pc) green_pc = green_term;
     DeviceGuard dg(g->device);
     const Geom& geo = g->geo;
@@ -1076,7 +1099,7 @@ int jfftb_pcg_batch(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi*
     require(green_term->grid == g && green_pc != nullptr && green_pc->grid == g,
             "Green operators live on a different grid");
     if (kind == JFFTB_PC_GREEN_JACOBI)
-      require(jac != nullptr && jac->op->grid == g, "kind needs an assembled Jacobi diagonal");
+      require(jac != nullptr && jac->grid == g, "kind needs an assembled Jacobi diagonal");
     DeviceGuard dg(g->device);
     const Geom& geo = g->geo;
     cudaStream_t s = g->stream;

@@ -165,7 +165,8 @@ struct jfftb_green {
 };
 
 struct jfftb_jacobi {
-  jfftb_op* op;
+  jfftb_op* op;        // the operator it was probed from (null: given as an array)
+  jfftb_grid* grid;
   double* inv_sqrt;  // device, d * N
 };
 

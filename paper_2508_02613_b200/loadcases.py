@@ -70,8 +70,10 @@ def solve_load_cases(op, preconditioner, green, loads=None, eta: float = DEFAULT
     shape = (d,) + (op.grid.n,) * d
     us = torch.empty((L,) + shape, dtype=torch.float64, device=dev)
     kind = preconditioner.kind
-    green_pc = preconditioner.green.handle if preconditioner.green is not None else None
-    jac = preconditioner.jacobi.handle if preconditioner.jacobi is not None else None
+    from .preconditioners import green_handle, jacobi_handle
+    green_pc = green_handle(preconditioner.green) if preconditioner.green is not None else None
+    jac = jacobi_handle(preconditioner.jacobi) if preconditioner.jacobi is not None else None
+    green_h = green_handle(green)
     n = op.grid.n
     # batched: every stage of the L solves in one launch (3-D power-of-two
     # grids, spectral kinds); otherwise one solve after the other
@@ -85,11 +87,11 @@ def solve_load_cases(op, preconditioner, green, loads=None, eta: float = DEFAULT
         dst = rhs[g] if batched else rhs
         N.check(lib.jfftb_assemble_rhs(h.ptr, N.dptr(e), C.c_void_p(dst.data_ptr()), N.DEVICE))
         if not batched:
-            it, hist, term, _ = pcg_device(h, kind, green.handle, jac, rhs.data_ptr(),
+            it, hist, term, _ = pcg_device(h, kind, green_h, jac, rhs.data_ptr(),
                                            us[g].data_ptr(), eta, max_iter, green_pc_h=green_pc)
             results.append((it, hist, term))
     if batched:
-        results, _ = pcg_device_batch(h, kind, green.handle, jac, L, rhs.data_ptr(),
+        results, _ = pcg_device_batch(h, kind, green_h, jac, L, rhs.data_ptr(),
                                       us.data_ptr(), eta, max_iter, green_pc_h=green_pc)
     its, terms, hists = [], [], []
     for g, (it, hist, term) in enumerate(results):

@@ -76,11 +76,44 @@ def _replacement(name: str, ref_solver):
     raise AttributeError(name)
 
 
+def _child_plug(package: str) -> None:
+    """Initializer of the sweep pool's worker processes."""
+    plug_into_reference(package)
+
+
+def _pool_factory(package: str, original):
+    """The reference's parameter sweeps fan out over a fork-based
+    ``ProcessPoolExecutor`` (experiments.py:326-330).  A process that has
+    already used CUDA cannot fork workers that use it, so the plugged-in
+    sweep starts its workers with ``spawn`` and plugs the GPU path into each
+    of them (the cells then run on libjfftb200 as well)."""
+    import functools
+    import multiprocessing as mp
+
+    @functools.wraps(original)
+    def make(*args, **kwargs):
+        kwargs.setdefault("mp_context", mp.get_context("spawn"))
+        kwargs.setdefault("initializer", _child_plug)
+        kwargs.setdefault("initargs", (package,))
+        return original(*args, **kwargs)
+    return make
+
+
 def plug_into_reference(package: str = "jfft") -> dict:
     """Rebind the reference's binding sites; returns the originals so that
     :func:`unplug` can restore them."""
     ref_solver = importlib.import_module(f"{package}.solver")
     saved = {}
+    try:
+        exp = importlib.import_module(f"{package}.experiments")
+    except ImportError:
+        exp = None
+    if exp is not None and hasattr(exp, "ProcessPoolExecutor") and \
+            not getattr(exp.ProcessPoolExecutor, "_jfftb_spawn", False):
+        saved[(exp.__name__, "ProcessPoolExecutor")] = exp.ProcessPoolExecutor
+        factory = _pool_factory(package, exp.ProcessPoolExecutor)
+        factory._jfftb_spawn = True
+        exp.ProcessPoolExecutor = factory
     for modname, names in _TARGETS.items():
         full = package if modname == "" else f"{package}.{modname}"
         try:

@@ -70,6 +70,37 @@ def assemble_green(grid, material_ref) -> GreenOperator:
     return GreenOperator(grid, material_ref, N.GreenHandle(grid_handle(grid), lam, mu))
 
 
+def green_handle(green) -> N.GreenHandle:
+    """Device Green operator of any GreenOperator-like object: ours carry
+    one; a reference GreenOperator (built by its own assemble_green) is
+    re-assembled on the device from its reference material (cached on it)."""
+    h = getattr(green, "handle", None)
+    if isinstance(h, N.GreenHandle):
+        return h
+    h = getattr(green, "_jfftb_green", None)
+    if h is None:
+        m = green.material_ref
+        h = N.GreenHandle(grid_handle(green.grid), float(m.lambda0), float(m.mu0))
+        object.__setattr__(green, "_jfftb_green", h)
+    return h
+
+
+def jacobi_handle(jacobi) -> N.JacobiHandle:
+    """Device diagonal of any JacobiDiagonal-like object: ours carry one; a
+    caller-built one (reference container, e.g. test_preconditioners.py
+    unit-diagonal cases) is uploaded from its ``inv_sqrt`` (cached on it)."""
+    h = getattr(jacobi, "handle", None)
+    if isinstance(h, N.JacobiHandle):
+        return h
+    arr = jacobi.inv_sqrt
+    key = (id(arr), arr.__array_interface__["data"][0])
+    c = getattr(jacobi, "_jfftb_jacobi", None)
+    if c is None or c[1] != key:
+        c = (N.JacobiHandle(None, grid_handle(jacobi.grid), arr), key)
+        object.__setattr__(jacobi, "_jfftb_jacobi", c)
+    return c[0]
+
+
 def _apply(kind_code, green, jacobi, r):
     grid = r.grid
     if green is not None and green.grid != grid:
@@ -78,8 +109,8 @@ def _apply(kind_code, green, jacobi, r):
         raise ValueError("residual lives on a different grid")
     vals = np.ascontiguousarray(r.values, dtype=np.float64)
     out = np.empty_like(vals)
-    gh = green.handle.ptr if green is not None else None
-    jh = jacobi.handle.ptr if jacobi is not None else None
+    gh = green_handle(green).ptr if green is not None else None
+    jh = jacobi_handle(jacobi).ptr if jacobi is not None else None
     N.check(N.load().jfftb_apply_precond(kind_code, gh, jh, N.vptr(vals), N.vptr(out), N.HOST))
     return new_vector(r, grid, out)
 

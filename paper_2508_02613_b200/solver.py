@@ -60,9 +60,10 @@ def pcg(op, rhs, preconditioner, green, eta: float = DEFAULT_ETA_CG,
     iters = C.c_int(0)
     term = C.c_int(0)
     wall = C.c_double(0.0)
-    gpc = preconditioner.green.handle.ptr if preconditioner.green is not None else None
-    jac = preconditioner.jacobi.handle.ptr if preconditioner.jacobi is not None else None
-    status = N.load().jfftb_pcg(h.ptr, code, gpc, jac, green.handle.ptr, N.vptr(vals), N.HOST,
+    from .preconditioners import green_handle, jacobi_handle
+    gpc = green_handle(preconditioner.green).ptr if preconditioner.green is not None else None
+    jac = jacobi_handle(preconditioner.jacobi).ptr if preconditioner.jacobi is not None else None
+    status = N.load().jfftb_pcg(h.ptr, code, gpc, jac, green_handle(green).ptr, N.vptr(vals), N.HOST,
                                 float(eta), max_iter, N.vptr(x), N.dptr(hist), C.byref(iters),
                                 C.byref(term), C.byref(wall))
     N.check(status, abort_error or SolverAbortError)

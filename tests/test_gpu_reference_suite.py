@@ -1,0 +1,50 @@
+"""The reference's own test suite (pkg/tests: 159 tests incl. the ten
+acceptance criteria, the sweeps on a worker pool and topology optimisation)
+with the GPU path plugged into the reference package
+(paper_2508_02613_b200.plugin; runner: tests/run_reference_suite.py).
+
+Three tests do not pass, and each is accounted for:
+* test_criterion_9_topopt_iteration_gap and
+  test_trend_laminate_saturation_at_low_contrast fail on the CPU reference
+  itself, unplugged (measured in this build container: criterion 9 reports
+  last-20% medians green-jacobi 34 / green 16 against the required 3x gap --
+  the plugged-in run gives 31 / 16; the saturation trend gives 13 vs 14
+  iterations for p = 32 vs 64 on both);
+* test_jacobi_uses_exactly_eight_probes counts calls of the reference's
+  module-level ``apply_system`` during ``assemble_jacobi``; the device
+  diagonal runs its d 2^d comb probes inside the library (jfftb_jacobi_create),
+  so that Python hook is never called.
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+REF_TESTS = os.path.join(REPO, "baseline", "_ref", "tests")
+
+EXPECTED_NOT_PASSING = {
+    "tests/test_acceptance.py::test_criterion_9_topopt_iteration_gap",
+    "tests/test_acceptance.py::test_trend_laminate_saturation_at_low_contrast",
+    "tests/test_preconditioners.py::test_jacobi_uses_exactly_eight_probes",
+}
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_TESTS),
+                    reason="reference not installed (baseline/install_ref.sh)")
+def test_reference_suite_through_plugin():
+    # a fresh process: the plugged-in sweeps start spawn workers, and the
+    # reference's tests must import jfft only after the plug-in is applied
+    r = subprocess.run([sys.executable, os.path.join(HERE, "run_reference_suite.py")],
+                       cwd=REPO, capture_output=True, text=True, timeout=1800)
+    out = os.path.join(REPO, "gpurun_out", "reference_suite.json")
+    outcomes = json.load(open(out))
+    not_passed = {k for k, v in outcomes.items() if v != "passed"}
+    assert len(outcomes) >= 150, r.stdout[-2000:]
+    assert not_passed == EXPECTED_NOT_PASSING, (not_passed, r.stdout[-3000:])
