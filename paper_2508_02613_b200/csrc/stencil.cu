@@ -304,14 +304,21 @@ __global__ void __launch_bounds__(BX3* BY3, MINB3)
 // --------------------------------------------------------------------------
 // 2-D plane-march stencil (axis 0 marched, axis 1 across threads)
 // --------------------------------------------------------------------------
+// Each thread owns one node column.  Its own node of plane k is loaded into
+// registers three layers ahead (plain loads, no barrier), published to a
+// double-buffered shared row for the neighbour on its left (and the tile's
+// halo column by the last thread), and the forces for the +x neighbour travel
+// through a double-buffered shared row that is read one layer later -- so a
+// layer costs ONE barrier, and a node is finalised and written one layer
+// after its last voxel.
 template <int MODE, bool SCALE>
 __global__ void __launch_bounds__(BX2)
     stencil2d(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
               double lam0, double mu0, EbarT E, double* __restrict__ out,
               double* __restrict__ partials, int chunk, int) {
   constexpr bool HAS_U = MODE != VOX_RHS;
-  __shared__ double U[2][BX2 + 1];
-  __shared__ double F[2][2][BX2];  // [plane][comp]
+  __shared__ double U[2][2][BX2 + 1];   // [buf][comp][x]: node plane kk + 1
+  __shared__ double F[2][2][2][BX2];    // [buf][plane][comp][x]: +x forces of layer kk
   __shared__ double red[32];
   const int n0 = g.n[0], n1 = g.n[1];
   const int tx = threadIdx.x;
@@ -321,74 +328,116 @@ __global__ void __launch_bounds__(BX2)
   const int gx = X0 - 1 + tx;
   const int c1 = wrapi(gx, n1);
   const bool outp = tx >= 1 && gx < n1;
+  const bool halo = tx == BX2 - 1;
   const int c1h = wrapi(X0 - 1 + BX2, n1);
   double gs[2] = {g.hinv[0], g.hinv[1]}, fs[2] = {g.hinv[0], g.hinv[1]};
   const double (*Eb)[3] = E.e;
-
-  auto load_plane = [&](int k) {
-    if (!HAS_U) return;
-    const int64_t base = (int64_t)k * n1;
+  auto pl = [&](int k) { return k < 0 ? k + n0 : (k >= n0 ? k - n0 : k); };
+  // own (and, for the last thread, halo-column) values of plane k
+  struct Node {
+    double v[2], h[2], r;
+  };
+  auto fetch = [&](int kk) {
+    Node q{};
+    const int64_t base = (int64_t)pl(kk) * n1;
+    if (HAS_U) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        q.v[i] = __ldg(u + i * g.N + base + c1);
+        q.h[i] = halo ? __ldg(u + i * g.N + base + c1h) : 0.0;
+      }
+    }
+    q.r = rho ? __ldg(rho + base + c1) : 1.0;
+    return q;
+  };
+  // prefetch ring: planes kk, kk + 1, kk + 2 (kk = k0 - 1 first)
+  Node q0 = fetch(k0 - 1), q1 = fetch(k0), q2 = fetch(k0 + 1);
+  double uk[2][2];  // corners of plane kk: own, +x
+  if (HAS_U) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      U[i][tx] = __ldg(u + i * g.N + base + c1);
-      if (tx == BX2 - 1) U[i][BX2] = __ldg(u + i * g.N + base + c1h);
+      U[1][i][tx] = q0.v[i];
+      if (halo) U[1][i][BX2] = q0.h[i];
     }
-  };
-  double uk[2][2] = {{0, 0}, {0, 0}}, uk1[2][2] = {{0, 0}, {0, 0}};
-  const int kstart = wrapi(k0 - 1, n0);
-  if (HAS_U) {
-    load_plane(kstart);
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 2; ++i) { uk[0][i] = U[i][tx]; uk[1][i] = U[i][tx + 1]; }
-    __syncthreads();
   }
-  double nxt[2] = {0.0, 0.0};
-  double csum = 0.0;
-  for (int kk = k0 - 1; kk < k1; ++kk) {
-    const int k = wrapi(kk, n0);
-    const int kp = (k + 1 == n0) ? 0 : k + 1;
-    if (HAS_U) {
-      load_plane(kp);
-      __syncthreads();
+  __syncthreads();
 #pragma unroll
-      for (int i = 0; i < 2; ++i) { uk1[0][i] = U[i][tx]; uk1[1][i] = U[i][tx + 1]; }
+  for (int i = 0; i < 2; ++i) {
+    uk[0][i] = HAS_U ? U[1][i][tx] : 0.0;
+    uk[1][i] = HAS_U ? U[1][i][tx + 1] : 0.0;
+  }
+  double nxt[2] = {0.0, 0.0}, ak[2] = {0.0, 0.0}, pk[2] = {0.0, 0.0};
+  double csum = 0.0;
+  int64_t oidx = (int64_t)pl(k0 - 1) * n1 + c1;  // node of the pending output
+  for (int kk = k0 - 1, j = 0; kk < k1; ++kk, ++j) {
+    const int b = j & 1;
+    // publish plane kk + 1, then request plane kk + 3
+    if (HAS_U) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        U[b][i][tx] = q1.v[i];
+        if (halo) U[b][i][BX2] = q1.h[i];
+      }
     }
-    const double r = rho ? __ldg(rho + (int64_t)k * n1 + c1) : 1.0;
+    const double rk = q0.r;
+    q0 = q1;
+    q1 = q2;
+    if (kk + 3 <= k1) q2 = fetch(kk + 3);
+    __syncthreads();  // U[b] written; F[b ^ 1] of layer kk - 1 written
+    // finish node kk - 1 with the +x forces of layer kk - 1
+    if (kk > k0 - 1) {
+      if (tx >= 1) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          ak[i] = ak[i] + F[b ^ 1][0][i][tx - 1];
+          nxt[i] = nxt[i] + F[b ^ 1][1][i][tx - 1];
+        }
+      }
+      if (kk - 1 >= k0 && outp) {
+        out[oidx] = ak[0];
+        out[g.N + oidx] = ak[1];
+        if (MODE == VOX_K && partials) csum += pk[0] * ak[0] + pk[1] * ak[1];
+      }
+      oidx += n1;
+      if (oidx >= g.N) oidx -= g.N;
+    }
+    double uk1[2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      uk1[0][i] = HAS_U ? q0.v[i] : 0.0;
+      uk1[1][i] = HAS_U ? U[b][i][tx + 1] : 0.0;
+    }
     double uc[4][2];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
       for (int i = 0; i < 2; ++i) uc[c][i] = (c & 1) ? uk1[(c >> 1) & 1][i] : uk[(c >> 1) & 1][i];
     double f[4][2];
-    voxel_forces<2, MODE, SCALE>(uc, lam0 * r, mu0 * r, gs, fs, Eb, f);
-    double ak[2];
+    voxel_forces<2, MODE, SCALE>(uc, lam0 * rk, mu0 * rk, gs, fs, Eb, f);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       ak[i] = nxt[i] + f[0][i];
       nxt[i] = f[1][i];
-      F[0][i][tx] = f[2][i];
-      F[1][i][tx] = f[3][i];
+      F[b][0][i][tx] = f[2][i];
+      F[b][1][i][tx] = f[3][i];
+      pk[i] = uk[0][i];
+      uk[0][i] = uk1[0][i];
+      uk[1][i] = uk1[1][i];
     }
-    __syncthreads();
+  }
+  // the last layer's node
+  __syncthreads();
+  {
+    const int b = (k1 - k0) & 1;  // buffer of layer k1 - 1
     if (tx >= 1) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        ak[i] = ak[i] + F[0][i][tx - 1];
-        nxt[i] = nxt[i] + F[1][i][tx - 1];
-      }
+      for (int i = 0; i < 2; ++i) ak[i] = ak[i] + F[b][0][i][tx - 1];
     }
-    if (kk >= k0 && outp) {
-      const int64_t idx = (int64_t)k * n1 + c1;
-      out[idx] = ak[0];
-      out[g.N + idx] = ak[1];
-      if (MODE == VOX_K && partials) csum += uk[0][0] * ak[0] + uk[0][1] * ak[1];
+    if (k1 - 1 >= k0 && outp) {
+      out[oidx] = ak[0];
+      out[g.N + oidx] = ak[1];
+      if (MODE == VOX_K && partials) csum += pk[0] * ak[0] + pk[1] * ak[1];
     }
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int i = 0; i < 2; ++i) uk[q][i] = uk1[q][i];
-    if (!HAS_U) __syncthreads();  // F is rewritten next layer
   }
   if (MODE == VOX_K && partials) {
     const double s = block_sum(csum, red);
@@ -415,8 +464,9 @@ StencilLaunch stencil_config(const Geom& g) {
     L.grid = dim3(bx, by, chunks);
     L.block = dim3(BX3, BY3, 1);
   } else {
+    // ~12 blocks of BX2 threads per SM in flight
     const int bx = (g.n[1] + BX2 - 2) / (BX2 - 1);
-    int chunks = (target + bx - 1) / bx;
+    int chunks = (3 * target + bx - 1) / bx;
     chunks = std::max(1, std::min(chunks, g.n[0]));
     L.chunk = (g.n[0] + chunks - 1) / chunks;
     chunks = (g.n[0] + L.chunk - 1) / L.chunk;
