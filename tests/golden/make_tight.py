@@ -137,9 +137,15 @@ def run(case: str) -> None:
            "eps_bar": eb, "lam": lam, "mu": mu, "sample": s}
     kinds = ("green-jacobi",) if big else (("green-jacobi", "green") if case.startswith("c5")
                                            else ("green", "green-jacobi"))
-    # config 5 (contrast 1e6): Green converges to the tight tolerance only
-    # after thousands of iterations -- its tight solve is skipped
-    skip_tight = {"green"} if case.startswith("c5") else set()
+    # tight solves that take thousands of oracle iterations are skipped (the
+    # discrete solution is the same for both kinds, so the tests hold the
+    # other kind's tight solution against both): config 5 Green (1658
+    # iterations, contrast 1e6) and config 3 Green-Jacobi (3046)
+    skip_tight = {"c5n128": {"green"}, "c3": {"green-jacobi"}}.get(case, set())
+    path = os.path.join(HERE, f"tight_{case}.npz")
+
+    def save():  # after every kind: a long run keeps what it has
+        np.savez_compressed(path, **{k: np.asarray(v) for k, v in out.items()})
     for kind in kinds:
         t = time.perf_counter()
         cap = 10 if big else FIXED[d]
@@ -156,6 +162,7 @@ def run(case: str) -> None:
               f"hist {out[f'{kind}_fixed_floor_hist']:.2e} ({time.perf_counter() - t:.0f}s)",
               flush=True)
         if big:
+            save()
             continue
         t = time.perf_counter()
         it, hist, term, x, sig = solver.solve(kind, 1e-6, 999)
@@ -164,6 +171,7 @@ def run(case: str) -> None:
         out[f"{kind}_std_hist"] = hist
         print(f"  {kind} eta=1e-6: {it} {term} ({time.perf_counter() - t:.0f}s)", flush=True)
         if kind in skip_tight:
+            save()
             continue
         t = time.perf_counter()
         eta = TIGHT * hist[0]
@@ -178,6 +186,7 @@ def run(case: str) -> None:
         out[f"{kind}_tight_fsum_iters"] = itf
         out[f"{kind}_tight_floor_u"] = np.abs(xf - x).max() / np.abs(x).max()
         out[f"{kind}_tight_floor_sigma"] = np.abs(sf - sig).max() / np.abs(sig).max()
+        save()
         print(f"  {kind} tight {it} ({itf} fsum) {term}: floor u "
               f"{out[f'{kind}_tight_floor_u']:.2e} sigma {out[f'{kind}_tight_floor_sigma']:.2e} "
               f"({time.perf_counter() - t:.0f}s)", flush=True)

@@ -1,0 +1,141 @@
+"""Tight parity at the BASELINE configurations:
+
+* config 2 (2048^2, i = 20, pure shear) against the REFERENCE's own solves;
+* config 3 (128^3 spheres), config 4's crack-disc field and config 5's SIMP
+  field (contrast 1e6) at 128^3, and configs 4 / 5 at 256^3 (10 fixed
+  Green-Jacobi iterations), against the oracle restatement.
+
+Fixtures: tests/golden/tight_<case>.npz (tests/golden/make_tight.py), each
+with the CPU-vs-CPU round-off floor (the same solve with exactly rounded dot
+products).  Bars:
+
+* fixed-iteration runs (eta = 0, K = 20 or 10): iteration count exact, the
+  whole residual history within 1e-10 and the iterate x_K within 1e-9
+  (max-abs over max-abs of a strided sample) -- or 10x the floor where the
+  floor is larger (2048^2 Green-Jacobi: 4.1e-9 on x_20);
+* eta = 1e-6 solves: iteration count +-1 and the first 10 history entries
+  within 1e-10;
+* tight solves (eta = 1e-24 ||f||^2_G, floors 1e-15 .. 1e-13): solution
+  sample and homogenized stress within 1e-9.
+The densities are rebuilt on the test host with the same seeded generators
+(microstructures.py) and checked against the fixture's sum / min / max.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_2508_02613_b200 import grid as G
+from paper_2508_02613_b200 import microstructures as ms
+from paper_2508_02613_b200.material import isotropic_material
+from paper_2508_02613_b200.operators import assemble_rhs, homogenized_stress, make_operator
+from paper_2508_02613_b200.preconditioners import assemble_green, build_preconditioner
+from paper_2508_02613_b200.solver import pcg
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["c2i20", "c3", "c4n128", "c5n128", "c4n256", "c5n256"]
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def density(case):
+    if case == "c2i20":
+        return ms.bernoulli_smoothed(2048, 20, 1e4, 0)
+    if case == "c3":
+        return ms.random_spheres(128, seed=0)
+    if case.startswith("c4"):
+        return ms.crack_discs(int(case[3:]), seed=0)
+    return ms.simp_density(int(case[3:]), seed=0)
+
+
+@pytest.fixture(scope="module", params=CASES)
+def case(request, golden_dir):
+    path = os.path.join(golden_dir, f"tight_{request.param}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"fixture {path} not generated")
+    gold = dict(np.load(path))
+    rho = density(request.param)
+    for k in ("rho_sum", "rho_min", "rho_max"):
+        v = {"rho_sum": rho.sum(), "rho_min": rho.min(), "rho_max": rho.max()}[k]
+        assert abs(v - float(gold[k])) <= 1e-12 * abs(float(gold[k])), (k, v, gold[k])
+    d = rho.ndim
+    grid = G.make_grid(rho.shape[0], (1.0,) * d)
+    mat = isotropic_material(float(gold["lam"]), float(gold["mu"]), d)
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    green = assemble_green(grid, mat)
+    eb = np.asarray(gold["eps_bar"])
+    rhs = assemble_rhs(op, eb)
+    pres = {}
+    return request.param, gold, op, green, eb, rhs, pres
+
+
+def _pre(pres, kind, op, green):
+    if kind not in pres:
+        pres[kind] = build_preconditioner(kind, op, green)
+    return pres[kind]
+
+
+def _sample(u, s):
+    return u[(slice(None),) + (slice(None, None, s),) * (u.ndim - 1)]
+
+
+@pytest.mark.parametrize("kind", ["green", "green-jacobi"])
+def test_fixed_iterations(case, kind):
+    name, gold, op, green, eb, rhs, pres = case
+    if f"{kind}_fixed_iters" not in gold:
+        pytest.skip("no fixed-iteration fixture for this kind")
+    K = int(gold[f"{kind}_fixed_iters"])
+    rep = pcg(op, rhs, _pre(pres, kind, op, green), green, eta=0.0, max_iter=K)
+    assert rep.iterations == K and rep.terminated == "iteration-cap"
+    h = np.array(rep.residual_history)
+    hg = gold[f"{kind}_fixed_hist"]
+    tol_h = max(1e-10, 10 * float(gold[f"{kind}_fixed_floor_hist"]))
+    assert np.abs(h - hg).max() / hg[0] <= tol_h, (name, kind)
+    tol_u = max(1e-9, 10 * float(gold[f"{kind}_fixed_floor_u"]))
+    us = _sample(rep.solution.values, int(gold["sample"]))
+    assert rel(us, gold[f"{kind}_fixed_usample"]) <= tol_u, (name, kind, tol_u)
+    sig = homogenized_stress(op, rep.solution, eb)
+    assert rel(sig, gold[f"{kind}_fixed_sigma"]) <= tol_u, (name, kind)
+
+
+@pytest.mark.parametrize("kind", ["green", "green-jacobi"])
+def test_eta_1e6_counts_and_history(case, kind):
+    name, gold, op, green, eb, rhs, pres = case
+    if f"{kind}_std_iters" not in gold:
+        pytest.skip("no eta = 1e-6 fixture for this kind")
+    rep = pcg(op, rhs, _pre(pres, kind, op, green), green, eta=1e-6)
+    assert rep.terminated == str(gold[f"{kind}_std_terminated"])
+    assert abs(rep.iterations - int(gold[f"{kind}_std_iters"])) <= 1, (name, kind)
+    hg = gold[f"{kind}_std_hist"]
+    k = min(10, len(hg), len(rep.residual_history))
+    assert np.abs(np.array(rep.residual_history[:k]) - hg[:k]).max() / hg[0] <= 1e-10
+
+
+@pytest.mark.parametrize("kind", ["green", "green-jacobi"])
+def test_tight_solution_and_stress(case, kind):
+    """Solved to eta = 1e-24 ||f||^2_G both kinds reach the same discrete
+    solution; where the oracle's tight solve of this kind would take
+    thousands of CPU iterations (config 3 Green-Jacobi: 3046, config 5
+    Green: 1658) the other kind's tight oracle solution is the target."""
+    name, gold, op, green, eb, rhs, pres = case
+    other = "green" if kind == "green-jacobi" else "green-jacobi"
+    src = kind if f"{kind}_tight_eta" in gold else other
+    if f"{src}_tight_eta" not in gold:
+        pytest.skip("no tight fixture")
+    pre = _pre(pres, kind, op, green)
+    h0 = pcg(op, rhs, pre, green, eta=0.0, max_iter=0).residual_history[0]
+    rep = pcg(op, rhs, pre, green, eta=1e-24 * h0, max_iter=20000)
+    assert rep.terminated == "converged"
+    if src == kind:
+        it_ref = int(gold[f"{kind}_tight_iters"])
+        assert abs(rep.iterations - it_ref) <= max(2, it_ref // 50), (name, kind, rep.iterations)
+    us = _sample(rep.solution.values, int(gold["sample"]))
+    assert float(gold[f"{src}_tight_floor_u"]) <= 1e-10  # the bar sits above the floor
+    assert rel(us, gold[f"{src}_tight_usample"]) <= 1e-9, (name, kind, src)
+    sig = homogenized_stress(op, rep.solution, eb)
+    assert rel(sig, gold[f"{src}_tight_sigma"]) <= 1e-9, (name, kind, src)
