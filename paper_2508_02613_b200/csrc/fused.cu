@@ -519,7 +519,10 @@ constexpr bool kGStage = true;
 // GS: 0 Green planes read from global in the solve, 1 bulk-staged in shared
 // memory, 2 evaluated analytically (3-D, green_block)
 constexpr int passC_gp(int D, int GS) { return GS == 1 ? (D == 2 ? 4 : 9) : 0; }
-constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / 16); }
+#ifndef JF_PC_NTDIV
+#define JF_PC_NTDIV 16
+#endif
+constexpr int passC_nt(int D, int L, int F) { return nt_for(F * D * L / JF_PC_NTDIV); }
 constexpr int passC_bufd(int D, int L, int F, int GS = 1) {
   return F * D * padded_len<CPAD>(L) * 2 + passC_gp(D, GS) * L;
 }
@@ -931,6 +934,14 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
   JF_LAUNCHED();
 }
 
+#ifdef JF_FAST_BUILD  // A/B builds: the 128 and 512 instantiations only
+#define JF_SIZE_SWITCH(L, CALL)                   \
+  switch (L) {                                    \
+    case 128: { constexpr int LL = 128; CALL; break; } \
+    case 512: { constexpr int LL = 512; CALL; break; } \
+    default: throw Error(JFFTB_EINVAL, "fused FFT: unsupported size (fast build)"); \
+  }
+#else
 #define JF_SIZE_SWITCH(L, CALL)                   \
   switch (L) {                                    \
     case 16: { constexpr int LL = 16; CALL; break; }   \
@@ -943,6 +954,7 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
     case 2048: { constexpr int LL = 2048; CALL; break; } \
     default: throw Error(JFFTB_EINVAL, "fused FFT: unsupported size"); \
   }
+#endif
 
 void launchA(const FGeom& g, cudaStream_t s, int F, int mode, const PcgState* st, double* r,
              const double* kp, const double* dinv, double2* spec, const double2* tw) {
