@@ -476,9 +476,13 @@ void fused_stage_B_slab(const Geom& geo, const SpecSlab& sl, cudaStream_t s, boo
 int fused_stage_C_slab(const Geom& geo, const SpecSlab& sl, cudaStream_t s, int F,
                        const PcgState* st, const double* green, double2* recv, double* partials,
                        const double2* tw);
+// comp >= 0: that component only
 void fused_stage_I_ext(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                        const double2* zspec, const double* dinv, double* p_ext, double* x,
-                       const double2* tw);
+                       const double2* tw, int comp = -1);
+void fused_stage_A_comp(const Geom& geo, cudaStream_t s, int F, int mode, const PcgState* st,
+                        double* r, const double* kp, const double* dinv, double2* spec,
+                        const double2* tw, int comp);
 // PCG scalar kernels (pcg.cu) over `count` partials: alpha = rz / curvature,
 // and the termination test / beta (solver.py:115-135)
 // (partial j of block b at partials[b * stride + j])

@@ -249,6 +249,12 @@ struct jfftb_dist {
   Geom gl{};      // one rank's real-space slab (n0, L1, n2)
   Geom gg{};      // the global grid
   cudaStream_t stream = nullptr;
+  // exchange stream: the per-component all-to-alls run here, gated by events,
+  // while `stream` transforms the next component (precond_phase)
+  cudaStream_t xstream = nullptr;
+  cudaEvent_t ev_c[3] = {nullptr, nullptr, nullptr};  // component c computed (stream)
+  cudaEvent_t ev_x[3] = {nullptr, nullptr, nullptr};  // component c exchanged (xstream)
+  bool overlap = true;
   double2* tw = nullptr;
   double* shared_gath = nullptr;  // loopback: the all-gather buffer all ranks share
   PcgState* host_st = nullptr;
@@ -262,6 +268,11 @@ struct jfftb_dist {
     if (shared_gath) cudaFree(shared_gath);
     if (tw) cudaFree(tw);
     if (host_st) cudaFreeHost(host_st);
+    for (int c = 0; c < 3; ++c) {
+      if (ev_c[c]) cudaEventDestroy(ev_c[c]);
+      if (ev_x[c]) cudaEventDestroy(ev_x[c]);
+    }
+    if (xstream) cudaStreamDestroy(xstream);
     if (stream) cudaStreamDestroy(stream);
   }
   int nf() const { return kind == JFFTB_PC_GREEN_JACOBI ? 6 : 3; }
@@ -287,9 +298,9 @@ struct P2P {
 // a batch of point-to-point transfers between ranks.  Loopback: device copies
 // (both ends are in this process).  NCCL: the local rank's sends and receives
 // in one group (self transfers are copies).
-void run_p2p(jfftb_dist* D, const std::vector<P2P>& xs) {
+void run_p2p(jfftb_dist* D, const std::vector<P2P>& xs, cudaStream_t s = nullptr) {
   jfftb_comm* c = D->comm;
-  cudaStream_t s = D->stream;
+  if (!s) s = D->stream;
   if (c->local) {
     for (const auto& x : xs)
       if (x.bytes && x.src != x.dst)
@@ -374,7 +385,8 @@ double* f_rho(Rank& r) { return r.rho_ext; }
 
 // forward all-to-all: rank r's pass-A spectra rows [k0lo_q, +kcnt_q) of
 // every field -> rank q's segment r
-void alltoall_fwd(jfftb_dist* D) {
+// (the fields of component c: c, and d + c for green-jacobi; c < 0: all)
+void alltoall_fwd(jfftb_dist* D, int c = -1, cudaStream_t s = nullptr) {
   const int P = D->P, nf = D->nf();
   const int64_t PSl = D->PSl(), CSl = (int64_t)D->K0() * PSl;
   std::vector<P2P> xs;
@@ -385,16 +397,19 @@ void alltoall_fwd(jfftb_dist* D) {
       if (!R && !Q) continue;
       const int k0lo = D->k0lo_of(q), kc = D->kcnt_of(q);
       const int64_t FS = (int64_t)kc * PSl, SS = nf * FS;
-      for (int f = 0; f < nf; ++f)
+      for (int f = 0; f < nf; ++f) {
+        if (c >= 0 && f % 3 != c) continue;
         xs.push_back({r, q, R ? R->spec + f * CSl + (int64_t)k0lo * PSl : nullptr,
                       Q ? Q->recv + r * SS + f * FS : nullptr, sizeof(double2) * FS});
+      }
     }
-  run_p2p(D, xs);
+  run_p2p(D, xs, s);
 }
 
 // backward: rank q's z^ fields (comps zq.. zq + 2) of segment r -> rank r's
 // spectra rows [k0lo_q, +kcnt_q)
-void alltoall_bwd(jfftb_dist* D, int zq) {
+// (component cc of z^ only when cc >= 0)
+void alltoall_bwd(jfftb_dist* D, int zq, int cc = -1, cudaStream_t s = nullptr) {
   const int P = D->P, nf = D->nf();
   const int64_t PSl = D->PSl(), CSl = (int64_t)D->K0() * PSl;
   std::vector<P2P> xs;
@@ -405,42 +420,90 @@ void alltoall_bwd(jfftb_dist* D, int zq) {
       if (!R && !Q) continue;
       const int k0lo = D->k0lo_of(q), kc = D->kcnt_of(q);
       const int64_t FS = (int64_t)kc * PSl, SS = nf * FS;
-      for (int c = 0; c < 3; ++c)
+      for (int c = 0; c < 3; ++c) {
+        if (cc >= 0 && c != cc) continue;
         xs.push_back({q, r, Q ? Q->recv + r * SS + (zq + c) * FS : nullptr,
                       R ? R->spec + (zq + c) * CSl + (int64_t)k0lo * PSl : nullptr,
                       sizeof(double2) * FS});
+      }
     }
-  run_p2p(D, xs);
+  run_p2p(D, xs, s);
 }
 
 // one PCG phase after the stencil: A, exchange, B, C, gather, finalize, B',
-// exchange, I  (INIT: the k = 0 pass, no update)
+// exchange, I  (INIT: the k = 0 pass, no update).
+//
+// With more than one rank the two all-to-alls are pipelined against the
+// passes on either side, component by component: pass A of component c + 1
+// runs while component c's spectra travel (exchange stream, gated by events),
+// pass B starts on the fields of a component as soon as they have landed,
+// and on the way back pass B' / the exchange / pass I of the three z^
+// components overlap the same way.  Only pass C needs every field.  The data
+// and the arithmetic are those of the unpipelined schedule (JFFTB_DIST_OVERLAP=0),
+// so the results are bitwise the same.
 void precond_phase(jfftb_dist* D, bool init) {
   const bool GJ = D->kind == JFFTB_PC_GREEN_JACOBI;
   const int F = GJ ? 2 : 1, d = 3;
   cudaStream_t s = D->stream;
   const int mode = init ? FUSED_INIT : FUSED_ITER;
-  for (auto& rk : D->ranks)
-    fused_stage_A(D->gl, s, F, mode, rk.st, rk.rs, rk.kp, GJ ? rk.dinv : nullptr, rk.spec, D->tw,
-                  Batch{});
-  alltoall_fwd(D);
+  const bool ov = D->overlap && D->P > 1;
+  cudaStream_t sx = D->xstream;
+  const int zq = GJ ? d : 0;
+  const int64_t CSl = (int64_t)D->K0() * D->PSl();
+  if (ov) {
+    for (int c = 0; c < d; ++c) {
+      for (auto& rk : D->ranks)
+        fused_stage_A_comp(D->gl, s, F, mode, rk.st, rk.rs, rk.kp, GJ ? rk.dinv : nullptr, rk.spec,
+                           D->tw, c);
+      JF_CUDA(cudaEventRecord(D->ev_c[c], s));
+      JF_CUDA(cudaStreamWaitEvent(sx, D->ev_c[c], 0));
+      alltoall_fwd(D, c, sx);
+      JF_CUDA(cudaEventRecord(D->ev_x[c], sx));
+    }
+    for (int c = 0; c < d; ++c) {
+      JF_CUDA(cudaStreamWaitEvent(s, D->ev_x[c], 0));
+      for (auto& rk : D->ranks)
+        for (int f = 0; f < F; ++f)
+          fused_stage_B_slab(D->gg, D->slab(rk), s, false, rk.st, rk.recv, f * d + c, 1, D->tw);
+    }
+  } else {
+    for (auto& rk : D->ranks)
+      fused_stage_A(D->gl, s, F, mode, rk.st, rk.rs, rk.kp, GJ ? rk.dinv : nullptr, rk.spec, D->tw,
+                    Batch{});
+    alltoall_fwd(D);
+    for (auto& rk : D->ranks)
+      fused_stage_B_slab(D->gg, D->slab(rk), s, false, rk.st, rk.recv, 0, F * d, D->tw);
+  }
   for (auto& rk : D->ranks) {
-    const SpecSlab sl = D->slab(rk);
-    fused_stage_B_slab(D->gg, sl, s, false, rk.st, rk.recv, 0, F * d, D->tw);
-    const int cnt = fused_stage_C_slab(D->gg, sl, s, F, rk.st, rk.green, rk.recv, rk.part, D->tw);
+    const int cnt =
+        fused_stage_C_slab(D->gg, D->slab(rk), s, F, rk.st, rk.green, rk.recv, rk.part, D->tw);
     launch_sum_partials(s, rk.part, cnt, 2, rk.mine);
   }
   allgather(D);
-  for (auto& rk : D->ranks) {
-    launch_finalize(D->kind, init, s, rk.st, rk.gath, D->P, 4, rk.hist);
-    fused_stage_B_slab(D->gg, D->slab(rk), s, true, rk.st, rk.recv, GJ ? d : 0, d, D->tw);
+  for (auto& rk : D->ranks) launch_finalize(D->kind, init, s, rk.st, rk.gath, D->P, 4, rk.hist);
+  if (ov) {
+    for (int c = 0; c < d; ++c) {
+      for (auto& rk : D->ranks)
+        fused_stage_B_slab(D->gg, D->slab(rk), s, true, rk.st, rk.recv, zq + c, 1, D->tw);
+      JF_CUDA(cudaEventRecord(D->ev_c[c], s));
+      JF_CUDA(cudaStreamWaitEvent(sx, D->ev_c[c], 0));
+      alltoall_bwd(D, zq, c, sx);
+      JF_CUDA(cudaEventRecord(D->ev_x[c], sx));
+    }
+    for (int c = 0; c < d; ++c) {
+      JF_CUDA(cudaStreamWaitEvent(s, D->ev_x[c], 0));
+      for (auto& rk : D->ranks)
+        fused_stage_I_ext(D->gl, s, mode, rk.st, rk.spec + zq * CSl, GJ ? rk.dinv : nullptr,
+                          rk.p_ext, rk.x, D->tw, c);
+    }
+  } else {
+    for (auto& rk : D->ranks)
+      fused_stage_B_slab(D->gg, D->slab(rk), s, true, rk.st, rk.recv, zq, d, D->tw);
+    alltoall_bwd(D, zq);
+    for (auto& rk : D->ranks)
+      fused_stage_I_ext(D->gl, s, mode, rk.st, rk.spec + zq * CSl, GJ ? rk.dinv : nullptr,
+                        rk.p_ext, rk.x, D->tw);
   }
-  const int zq = GJ ? d : 0;
-  alltoall_bwd(D, zq);
-  const int64_t CSl = (int64_t)D->K0() * D->PSl();
-  for (auto& rk : D->ranks)
-    fused_stage_I_ext(D->gl, s, mode, rk.st, rk.spec + zq * CSl, GJ ? rk.dinv : nullptr,
-                      rk.p_ext, rk.x, D->tw);
 }
 
 void iteration(jfftb_dist* D) {
@@ -576,6 +639,12 @@ int jfftb_dist_create(jfftb_comm* comm, const int64_t* n, const double* lengths,
       D->gl = mk(D->L1);
       D->gg = mk(D->n[1]);
       JF_CUDA(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));
+      JF_CUDA(cudaStreamCreateWithFlags(&D->xstream, cudaStreamNonBlocking));
+      for (int c = 0; c < 3; ++c) {
+        JF_CUDA(cudaEventCreateWithFlags(&D->ev_c[c], cudaEventDisableTiming));
+        JF_CUDA(cudaEventCreateWithFlags(&D->ev_x[c], cudaEventDisableTiming));
+      }
+      if (const char* e = std::getenv("JFFTB_DIST_OVERLAP")) D->overlap = e[0] != '0';
       JF_CUDA(cudaMalloc(&D->tw, sizeof(double2) * kTwiddleN));
       launch_twiddles(D->stream, D->tw);
       JF_CUDA(cudaMallocHost(&D->host_st, sizeof(PcgState)));

@@ -74,6 +74,9 @@ struct FGeom {
   // state each; vector fields vs doubles and spectra bss complex apart
   int L;
   int64_t vs, bss;
+  // passes A and I: components [c0, c0 + nc) of this launch (dist.cu runs them
+  // component by component to overlap the all-to-all with the next one)
+  int c0, nc;
   __device__ __forceinline__ int64_t row_off(int64_t row) const {
     const int64_t k = row >> rsh;
     const int k1 = (int)(row & ((1 << rsh) - 1));
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(passA_nt(M, F, TW), passA_nt(M, F, TW) <= 512 
   static_assert(PE * NT == RAWN && PE % CH == 0, "pass A tiling");
   static_assert(F == 1 || MODE != FM_APPLY, "APPLY transforms one field");
   extern __shared__ double2 sbuf[];  // packed tile [k][field][col], k < M
-  const int c = blockIdx.y % g.d, bl = blockIdx.y / g.d;  // component, right-hand side
+  const int c = g.c0 + blockIdx.y % g.nc, bl = blockIdx.y / g.nc;  // component, right-hand side
   if (st) st += bl;
   r += bl * g.vs;
   if (kp) kp += bl * g.vs;
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(passA3_nt<M>(), 1)
   constexpr int Q0 = M / R0;
   static_assert(MODE == FM_ITER || MODE == FM_INIT, "pass A3 runs the PCG modes");
   extern __shared__ double2 sbuf[];   // [m][field][col]
-  const int c = blockIdx.y % g.d, bl = blockIdx.y / g.d;  // component, right-hand side
+  const int c = g.c0 + blockIdx.y % g.nc, bl = blockIdx.y / g.nc;  // component, right-hand side
   st += bl;
   r += bl * g.vs;
   kp += bl * g.vs;
@@ -709,7 +712,7 @@ __global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
   constexpr int TW = tw_a(M);
   constexpr int NT = passI_nt(M);
   extern __shared__ double2 sbuf[];  // [k][col], k <= M
-  const int c = blockIdx.y % g.d, bl = blockIdx.y / g.d;  // component, right-hand side
+  const int c = g.c0 + blockIdx.y % g.nc, bl = blockIdx.y / g.nc;  // component, right-hand side
   if (st) st += bl;
   zspec += bl * g.bss;
   if (p) p += bl * g.vs;
@@ -808,6 +811,8 @@ FGeom fgeom(const Geom& g) {
   f.L = 1;
   f.vs = 0;
   f.bss = 0;
+  f.c0 = 0;
+  f.nc = g.d;
   return f;
 }
 
@@ -820,7 +825,7 @@ void launchA_MT(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, c
   auto k = passA<M, F, MODE, TW>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  dim3 grid((unsigned)(g.PS / TW), g.d * g.L);
+  dim3 grid((unsigned)(g.PS / TW), g.nc * g.L);
   k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
   JF_LAUNCHED();
 }
@@ -851,7 +856,7 @@ void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, co
       auto k = passA3_fused_last() ? passA3<M, MODE, true> : passA3<M, MODE, false>;
       static std::atomic<uint64_t> attr{0};
       set_smem_once(k, smem, attr);
-      dim3 grid((unsigned)(g.PS / TW), g.d * g.L);
+      dim3 grid((unsigned)(g.PS / TW), g.nc * g.L);
       k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
       JF_LAUNCHED();
       return;
@@ -929,7 +934,7 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
   auto k = passI<M, MODE>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  dim3 grid((unsigned)(g.PS / TW), g.d * g.L);
+  dim3 grid((unsigned)(g.PS / TW), g.nc * g.L);
   k<<<grid, NT, smem, s>>>(g, st, zspec, dinv, p, x, out, tw);
   JF_LAUNCHED();
 }
@@ -1090,6 +1095,15 @@ void fused_stage_A(const Geom& geo, cudaStream_t s, int F, int mode, const PcgSt
                    const double2* tw, const Batch& bt) {
   launchA(fgeom_b(geo, bt), s, F, mode, st, r, kp, dinv, spec, tw);
 }
+// one component (dist.cu)
+void fused_stage_A_comp(const Geom& geo, cudaStream_t s, int F, int mode, const PcgState* st,
+                        double* r, const double* kp, const double* dinv, double2* spec,
+                        const double2* tw, int comp) {
+  FGeom g = fgeom(geo);
+  g.c0 = comp;
+  g.nc = 1;
+  launchA(g, s, F, mode, st, r, kp, dinv, spec, tw);
+}
 void fused_stage_B(const Geom& geo, cudaStream_t s, bool inv, const PcgState* st,
                    double2* spec, int ncomp, const double2* tw, const Batch& bt) {
   const FGeom g = fgeom_b(geo, bt);
@@ -1153,8 +1167,12 @@ int fused_stage_C_slab(const Geom& geo, const SpecSlab& sl, cudaStream_t s, int 
 // n1 + 2 rows along axis 1 (geo: the rank's local real-space slab)
 void fused_stage_I_ext(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                        const double2* zspec, const double* dinv, double* p_ext, double* x,
-                       const double2* tw) {
+                       const double2* tw, int comp) {
   FGeom g = fgeom(geo);
+  if (comp >= 0) {
+    g.c0 = comp;
+    g.nc = 1;
+  }
   g.pPS = (int64_t)(geo.n[1] + 2) * geo.n[2];
   g.pN = (int64_t)geo.n[0] * g.pPS;
   g.poff = geo.n[2];  // row 0 of the extended slab is the lower halo
