@@ -192,10 +192,13 @@ PcgBuffers pcg_workspace(jfftb_grid* g, int kcount, int max_iter) {
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t need_hist = sizeof(double) * (size_t)(max_iter + 1);
   const int64_t nspec = std::max<int64_t>(geo.Nh, spec_elems(g));
-  const int sblocks = std::max(kRedBlocks, kFusedMaxBlocks);
+  const bool bcb = g->fused && fused_bcb_supported(geo);
+  const int sblocks = (int)std::max<int64_t>(std::max(kRedBlocks, kFusedMaxBlocks),
+                                             bcb ? fused_bcb_partials(geo) : 0);
+  const size_t qbytes = sizeof(unsigned) * (2 + 2 * (size_t)(geo.n[0] / 2 + 1));
   const size_t fixed = al(sizeof(double) * n) * 3 + al(sizeof(double) * 2 * n) +
                        al(sizeof(double2) * 2 * geo.d * nspec) + al(sizeof(PcgState)) +
-                       al(sizeof(double) * (kcount + 2 * sblocks + kRedBlocks));
+                       al(sizeof(double) * (kcount + 2 * sblocks + kRedBlocks)) + al(qbytes);
   const size_t total = fixed + al(need_hist);
   if (g->ws_bytes < total) {
     if (g->ws) JF_CUDA(cudaFree(g->ws));
@@ -222,6 +225,8 @@ PcgBuffers pcg_workspace(jfftb_grid* g, int kcount, int max_iter) {
   B.spart = B.kpart + kcount;
   B.upart = B.spart + 2 * sblocks;
   B.kcount = kcount;
+  B.bcbq = bcb ? (unsigned*)take(qbytes) : nullptr;
+  if (!bcb) take(qbytes);
   B.hist = (double*)p;
   return B;
 }
@@ -296,7 +301,7 @@ void run_iteration_graph(jfftb_grid* g, int kind, jfftb_op* op, jfftb_jacobi* ja
                          jfftb_green* gpc, jfftb_green* gterm, const PcgBuffers& B) {
   constexpr int kIterKey = jfftb_grid::kIterKey;
   const void* key[kIterKey] = {op, op->rho, jac, jac ? jac->inv_sqrt : nullptr, gpc->blocks,
-                               gterm->blocks, B.x, B.st, B.hist, g->stream};
+                               gterm->blocks, B.x, B.st, B.hist, g->stream, B.bcbq};
   const double lame[6] = {op->lambda0, op->mu0, gpc->lambda_ref, gpc->mu_ref,
                           gterm->lambda_ref, gterm->mu_ref};
   bool hit = g->iter_graph != nullptr && g->iter_kind == kind;

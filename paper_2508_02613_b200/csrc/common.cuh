@@ -109,7 +109,7 @@ struct jfftb_grid {
   void* host_stage = nullptr;   // pinned staging ring for pageable host copies (hostio.cu)
   // one PCG iteration captured as a CUDA graph (api.cu jfftb_pcg), valid for
   // the key it was captured with
-  static constexpr int kIterKey = 10;
+  static constexpr int kIterKey = 11;
   cudaGraphExec_t iter_graph = nullptr;
   const void* iter_key[kIterKey] = {};
   // constants baked into the kernels' arguments: op Lame, Green (pc, term) Lame
@@ -422,6 +422,7 @@ struct PcgBuffers {
   double *kpart, *spart, *upart;
   int kcount;
   int hstride = 0;          // batched: history entries per right-hand side
+  unsigned* bcbq = nullptr; // merged pass B/C/B' work queue (fused.cu passBCB)
 };
 // batched right-hand sides: L solves, vector fields vs doubles apart,
 // spectra bss complex elements apart (L = 1: the plain solve)
@@ -462,6 +463,12 @@ int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const 
 void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                    const double2* zspec, const double* dinv, double* p, double* x,
                    const double2* tw, const Batch& bt);
+// passes B, C, B' as one persistent kernel (3-D, n1 == n2, one solve)
+bool fused_bcb_supported(const Geom& geo);
+int64_t fused_bcb_partials(const Geom& geo);  // partial pairs it writes
+int fused_stage_BCB(const Geom& geo, cudaStream_t s, int F, const PcgState* st,
+                    const jfftb_green* gpc_h, const jfftb_green* gterm_h, double2* spec,
+                    double* partials, const double2* tw, unsigned* q);
 
 int64_t fused_component_stride(const Geom& geo);
 // distributed solves (dist.cu): one rank's k0-slab of the spectral passes

@@ -183,7 +183,8 @@ __host__ __device__ constexpr int padded_len(int L) {
 // WARP: the calling warp alone transforms its sequences (NT = 32, lane-indexed,
 // __syncwarp between stages) -- no block-wide barrier
 // GIN: the first stage reads its inputs from global memory (sequence q
-// contiguous at gin + q * gqs) instead of buf; GOUT: the last stage writes
+// contiguous at gin + q * gqs; L2 loads, never through L1: the merged pass
+// B/C/B' reads rows other SMs wrote during the same launch) instead of buf; GOUT: the last stage writes
 // its outputs to gout + q * gqs (no trailing barrier -- buf is only read).
 template <int L, int NSEQ, int NT, bool INV, bool QFAST, int PAD, int S, int NS, bool WARP = false,
           bool GIN = false, bool GOUT = false, bool SEG = false>
@@ -230,7 +231,7 @@ __device__ __forceinline__ void cta_fft_stage(double2* buf, int ks, int qs,
         if constexpr (FROM_G) {
           const double2* src = gin + qq[m] * gqs;
 #pragma unroll
-          for (int t = 0; t < R; ++t) v[m][t] = src[gix(jj[m] + t * NB)];
+          for (int t = 0; t < R; ++t) v[m][t] = __ldcg(src + gix(jj[m] + t * NB));
         } else {
           const double2* src = buf + qq[m] * qs;
 #pragma unroll
@@ -366,7 +367,7 @@ __device__ __forceinline__ void cta_fft_ip_stage(double2* buf, int qs,
       if constexpr (FROM_G) {
         const double2* src = gin + q * gqs;
 #pragma unroll
-        for (int t = 0; t < R; ++t) v[t] = src[base + Q * t];
+        for (int t = 0; t < R; ++t) v[t] = __ldcg(src + base + Q * t);
       } else if constexpr (QF) {
 #pragma unroll
         for (int t = 0; t < R; ++t) v[t] = buf[(base + Q * t) * ks + q];

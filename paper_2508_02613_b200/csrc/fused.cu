@@ -693,6 +693,202 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
 }
 
 // ---------------------------------------------------------------------------
+// passes B, C and B' merged into one persistent kernel (3-D, one solve,
+// n1 == n2): the axis-1 transform of a k0-plane, the axis-2 transform / Green
+// block solve / inverse of its rows and the inverse axis-1 transform of its
+// z^ fields run back to back while the plane is still in L2 (one plane of
+// six fields is 24 MiB at 512^2; the 126 MB L2 holds the two or three planes
+// in flight), so the spectra cross HBM once on the way in and z^ once on the
+// way out instead of three round trips: 16.5 U of DRAM traffic instead of
+// 31.5 U for the three passes (green-jacobi, incl. 4.5 U of Green planes and
+// 3 U of write-back of the transformed r^ rows).
+//
+// Work items, claimed in order from a global ticket counter by the resident
+// CTAs:  stage s = 0 .. K0 holds  C(s-1): one frequency row-set of plane
+// s-1 | B(s): one (field, 8-column tile) axis-1 transform of plane s |
+// B'(s-1): one (z^ component, tile) inverse transform of plane s-1 -- so the
+// rows B(k) writes are re-read after only B'(k-1) (24 MiB of traffic at
+// 512^2) and z^(k) after B(k+1) (48 MiB): short reuse distances for the L2.
+// C(k) waits until all B(k) items have signalled (per-plane counter,
+// release/acquire at gpu scope), B'(k) until all C(k) items have.  A waiting
+// CTA only ever waits on items with smaller tickets, which running CTAs
+// hold, so the schedule cannot deadlock whatever the residency; by the time
+// a dependent item is claimed its producers were claimed a few hundred
+// tickets earlier.  Loads of rows written during the launch go to L2 (ld.cg, fft.cuh).
+// Every C item writes its own Parseval partial pair: the sums stay in a
+// fixed order (bitwise deterministic) although the item -> CTA map is not.
+// ---------------------------------------------------------------------------
+#ifndef JF_BCB_NT
+#define JF_BCB_NT 256
+#endif
+constexpr int BCB_NT = JF_BCB_NT;
+constexpr int bcb_bufd(int L, int F) {
+  return passC_bufd(3, L, F, 1) > 2 * tw_b(L) * L ? passC_bufd(3, L, F, 1) : 2 * tw_b(L) * L;
+}
+constexpr int bcb_minb(int L, int F) {
+  return bcb_bufd(L, F) * 8 <= 110 * 1024 ? 2 : 1;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int L, int F>
+__global__ void __launch_bounds__(BCB_NT, bcb_minb(L, F))
+    passBCB(FGeom g, const PcgState* __restrict__ st, const double* __restrict__ gpc,
+            const double* __restrict__ gterm, double2* __restrict__ spec,
+            double* __restrict__ partials, const double2* __restrict__ tw,
+            unsigned* __restrict__ q) {
+  constexpr int D = 3, NQ = F * D, NT = BCB_NT;
+  constexpr int TW = tw_b(L), NTILE = L / TW;
+  constexpr int RL = padded_len<CPAD>(L);
+  constexpr int GP = passC_gp(D, 1);
+  constexpr int ZQ = F == 2 ? D : 0;
+  extern __shared__ double2 sbuf[];
+  __shared__ double red[64];
+  __shared__ uint64_t gbar;
+  __shared__ unsigned s_ticket;
+  if (st->done) return;
+  const int K = g.K0;
+  const unsigned nB = NQ * NTILE, nC = (unsigned)(g.PS / L), nBi = D * NTILE;
+  const unsigned per = nB + nC + nBi, total = (unsigned)(K + 1) * per;
+  unsigned* cntB = q + 2;
+  unsigned* cntC = cntB + K;
+  const double invN = 1.0 / (double)g.N;
+  const int64_t Nh = g.CS;
+  double* gsm = reinterpret_cast<double*>(sbuf + NQ * RL);
+  unsigned gphase = 0;
+  if (threadIdx.x == 0) mbar_init(&gbar, 1);
+  // all of a producer item's stores, then (thread 0) fence + count
+  // (a release reduction: nobody waits for its round trip)
+  auto signal = [&](unsigned* cnt) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(cnt) : "memory");
+  };
+  // returns false if the producers never arrive (a bug guard, not a path)
+  auto wait_for = [&](const unsigned* cnt, unsigned need) {
+    if (threadIdx.x == 0) {
+      unsigned spins = 0;
+      while (ld_acquire_u32(cnt) < need) {
+        __nanosleep(32);
+        if (++spins > (1u << 24)) {
+          atomicExch(q + 1, 1u);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  };
+  // the next ticket is drawn while the current item runs
+  unsigned next = 0;
+  if (threadIdx.x == 0) next = atomicAdd(q, 1u);
+  for (;;) {
+    __syncthreads();  // the previous item is done with s_ticket and the tile
+    if (threadIdx.x == 0) s_ticket = next;
+    __syncthreads();
+    const unsigned t = s_ticket;
+    if (t >= total) break;
+    if (threadIdx.x == 0) next = atomicAdd(q, 1u);
+    const int s = (int)(t / per);
+    const unsigned o = t % per;
+    if (o >= nC && o < nC + nB) {
+      // ---- B(s): axis-1 transform of (field c, column tile) of plane s
+      const int k = s;
+      if (k >= K) continue;
+      const unsigned ob = o - nC;
+      const int c = (int)(ob / NTILE), tile = (int)(ob % NTILE);
+      double2* base = spec + c * g.FS + (int64_t)k * g.KS + (int64_t)tile * TW;
+      cta_fft_io<L, TW, NT, false, true, 0, true, true, false>(sbuf, TW, 1, tw, base, base, 1,
+                                                               g.nlast);
+      signal(cntB + k);
+    } else if (o < nC) {
+      // ---- C(s-1): one frequency row-set (F * 3 rows) of plane s - 1
+      const int k = s - 1;
+      if (k < 0 || k >= K) continue;
+      const int64_t row = (int64_t)k * nC + o;
+      const int64_t rbase = row * L;
+      const int k0 = g.k0lo + k;
+      const double w = (k0 == 0 || 2 * k0 == g.n0) ? 1.0 : 2.0;
+      if (threadIdx.x == 0) {
+        fence_proxy_async();  // earlier generic accesses of the tile come first
+        mbar_expect_tx(&gbar, GP * L * sizeof(double));
+#pragma unroll 1
+        for (int p = 0; p < GP; ++p)
+          bulk_g2s(gsm + p * L, gpc + p * Nh + rbase, L * sizeof(double), &gbar);
+      }
+      wait_for(cntB + k, nB);
+      cta_fft_dif<L, NQ, NT, CPAD, true>(sbuf, RL, tw, spec + rbase, g.FS);
+      mbar_wait(&gbar, gphase);
+      gphase ^= 1;
+      double q0 = 0.0, q1 = 0.0;
+#pragma unroll 1
+      for (int kk = threadIdx.x; kk < L; kk += NT) {
+        const int64_t f = rbase + kk;
+        HB<D> B;
+#pragma unroll
+        for (int a = 0; a < D; ++a) B.dg[a] = gsm[a * L + kk];
+#pragma unroll
+        for (int oo = 0; oo < 3; ++oo) {
+          B.re[oo] = gsm[(D + 2 * oo) * L + kk];
+          B.im[oo] = gsm[(D + 2 * oo + 1) * L + kk];
+        }
+        double2 sv[D], z[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) sv[a] = sbuf[(ZQ + a) * RL + pidx<CPAD>(kk)];
+        const double qs = hb_apply<D>(B, sv, z);
+        if (F == 2) {
+          double2 rr[D], tmp[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) rr[a] = sbuf[a * RL + pidx<CPAD>(kk)];
+          const double qr = (gterm == gpc) ? hb_apply<D>(B, rr, tmp)
+                                           : hb_apply<D>(ld_block<D>(gterm, Nh, f), rr, tmp);
+          q0 += w * qr;
+          q1 += w * qs;
+        } else {
+          q1 += w * qs;
+          if (gterm == gpc) {
+            q0 += w * qs;
+          } else {
+            double2 tmp[D];
+            q0 += w * hb_apply<D>(ld_block<D>(gterm, Nh, f), sv, tmp);
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) sbuf[(ZQ + a) * RL + pidx<CPAD>(kk)] = cscale(z[a], invN);
+      }
+      // this row-set's Parseval pair (fixed order: warp tree, then warps 0..7)
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      q0 = warp_sum(q0 * invN);
+      q1 = warp_sum(q1 * invN);
+      if (lane == 0) { red[wid] = q0; red[32 + wid] = q1; }
+      __syncthreads();  // block solve done: z^ rows complete, partials staged
+      if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) { a += red[i]; b += red[32 + i]; }
+        partials[2 * row] = a;
+        partials[2 * row + 1] = b;
+      }
+      cta_fft_dit_inv<L, D, NT, CPAD, true>(sbuf + ZQ * RL, RL, tw, spec + ZQ * g.FS + rbase,
+                                            g.FS);
+      signal(cntC + k);
+    } else {
+      // ---- B'(s-1): inverse axis-1 transform of (z^ component, tile) of plane s - 1
+      const int k = s - 1;
+      if (k < 0 || k >= K) continue;
+      const unsigned oo = o - nB - nC;
+      const int c = ZQ + (int)(oo / NTILE), tile = (int)(oo % NTILE);
+      wait_for(cntC + k, nC);
+      double2* base = spec + c * g.FS + (int64_t)k * g.KS + (int64_t)tile * TW;
+      cta_fft_io<L, TW, NT, true, true, 0, true, true, false>(sbuf, TW, 1, tw, base, base, 1,
+                                                              g.nlast);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // pass I: axis-0 complex-to-real of z^ fused with the PCG direction update.
 //   FM_ITER:  if alpha is valid: x += alpha p ; unless done: p = Dz + beta p
 //   FM_INIT:  p = Dz
@@ -925,6 +1121,29 @@ int launchC_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* 
     return launchC_V<D, L, F, MODE, 1, true>(g, s, st, gpc, gterm, spec, partials, tw, ga);
   return launchC_V<D, L, F, MODE, 1, false>(g, s, st, gpc, gterm, spec, partials, tw, ga);
 }
+template <int L, int F>
+int launchBCB_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double* gpc,
+                const double* gterm, double2* spec, double* partials, const double2* tw,
+                unsigned* q) {
+  constexpr int NT = BCB_NT;
+  const size_t smem = sizeof(double) * bcb_bufd(L, F);
+  auto k = passBCB<L, F>;
+  static std::atomic<uint64_t> attr{0};
+  static int per_sm_dev[64];
+  const int dev = current_device();
+  if (!(attr.load() & (1ull << dev))) {
+    set_smem_once(k, smem, attr);
+    JF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_dev[dev], k, NT, smem));
+  }
+  int sms = 0;
+  JF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int blocks = std::max(per_sm_dev[dev], 1) * sms;
+  JF_CUDA(cudaMemsetAsync(q, 0, sizeof(unsigned) * (2 + 2 * (size_t)g.K0), s));
+  k<<<blocks, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, q);
+  JF_LAUNCHED();
+  return (int)(g.CS / L);
+}
+
 template <int M, int MODE>
 void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2* zspec,
                const double* dinv, double* p, double* x, double* out, const double2* tw) {
@@ -1128,6 +1347,34 @@ int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const 
     return blocks;
   }
   return launchC(g, s, F, FM_ITER, st, gpc, gterm, spec, partials, tw, ga, an);
+}
+// Merged B / C / B' (passBCB): 3-D grids with n1 == n2, one solve, stored
+// Green planes.  Opt-in (JFFTB_BCB=1): it halves the DRAM traffic of the three
+// passes (ncu, 512^3 green-jacobi: 18.0 GB vs 33.8 GB per iteration) but runs
+// slower than them (7.9 vs 6.5 ms): with 92 KB of shared memory and 128
+// registers x 256 threads per item only two items fit an SM, and the items
+// are latency-bound (B 6.3 us, C 9.0 us, B' 5.0 us each), while the separate
+// passes each fill the SM for their own bottleneck (profiles/r02_ab_notes.md)
+bool fused_bcb_supported(const Geom& geo) {
+  const char* e = std::getenv("JFFTB_BCB");  // read per solve (tests switch it)
+  const bool on = e && e[0] != '0';
+  return on && geo.d == 3 && geo.n[1] == geo.n[2] && fused_supported(geo) && fused_dif() &&
+         !green_analytic_enabled();
+}
+int64_t fused_bcb_partials(const Geom& geo) {
+  return geo.d == 3 ? (int64_t)(geo.n[0] / 2 + 1) * geo.n[1] : 0;
+}
+// returns the number of partial pairs written; q: 2 + 2 K0 counters
+int fused_stage_BCB(const Geom& geo, cudaStream_t s, int F, const PcgState* st,
+                    const jfftb_green* gpc_h, const jfftb_green* gterm_h, double2* spec,
+                    double* partials, const double2* tw, unsigned* q) {
+  const FGeom g = fgeom(geo);
+  const double* gpc = gpc_h->blocks;
+  const double* gterm = gterm_h->blocks;
+  int n = 0;
+  if (F == 2) { JF_SIZE_SWITCH(g.nlast, (n = launchBCB_L<LL, 2>(g, s, st, gpc, gterm, spec, partials, tw, q))); }
+  else { JF_SIZE_SWITCH(g.nlast, (n = launchBCB_L<LL, 1>(g, s, st, gpc, gterm, spec, partials, tw, q))); }
+  return n;
 }
 void fused_stage_I(const Geom& geo, cudaStream_t s, int mode, const PcgState* st,
                    const double2* zspec, const double* dinv, double* p, double* x,

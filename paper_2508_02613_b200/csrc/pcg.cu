@@ -37,8 +37,18 @@ __device__ __forceinline__ double block_sum1(double v, double* red) {
 
 // fixed-order sum of partials[b*stride + j], b < count, in one 1024-thread block
 __device__ double sum_strided(const double* p, int count, int stride, int j, double* red) {
-  double s = 0.0;
-  for (int b = threadIdx.x; b < count; b += blockDim.x) s += p[(int64_t)b * stride + j];
+  // four independent running sums per thread (fixed order, loads in flight)
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int step = blockDim.x;
+  int b = threadIdx.x;
+  for (; b + 3 * step < count; b += 4 * step) {
+    a0 += p[(int64_t)b * stride + j];
+    a1 += p[(int64_t)(b + step) * stride + j];
+    a2 += p[(int64_t)(b + 2 * step) * stride + j];
+    a3 += p[(int64_t)(b + 3 * step) * stride + j];
+  }
+  for (; b < count; b += step) a0 += p[(int64_t)b * stride + j];
+  double s = (a0 + a1) + (a2 + a3);
   s = block_sum1(s, red);
   __syncthreads();
   return s;  // valid in thread 0
@@ -255,15 +265,22 @@ static void pcg_precond_phase_fused(jfftb_op* op, jfftb_grid* g, jfftb_jacobi* j
   constexpr bool GJ = KIND == JFFTB_PC_GREEN_JACOBI;
   constexpr bool SPECTRAL_PC = GJ || KIND == JFFTB_PC_GREEN;
   constexpr int F = GJ ? 2 : 1;
+  const bool bcb = SPECTRAL_PC && B.bcbq && fused_bcb_supported(geo);
   int scount;
   if (SPECTRAL_PC) {
     // r' = r - alpha Kp and its transform; green-jacobi adds s = D^-1/2 r'
     fused_stage_A(geo, s, F, INIT ? FUSED_INIT : FUSED_ITER, B.st, r, B.kp, dinv, B.spec, tw,
                   Batch{});
     if (!INIT) prof_mark(g);
-    fused_stage_B(geo, s, false, B.st, B.spec, F * geo.d, tw, Batch{});
-    if (!INIT) prof_mark(g);
-    scount = fused_stage_C(geo, s, F, false, B.st, gpc, gterm, B.spec, B.spart, tw, Batch{});
+    if (bcb) {
+      // B, C and B' in one persistent kernel (the "spectral" stage of the profile)
+      if (!INIT) prof_mark(g);
+      scount = fused_stage_BCB(geo, s, F, B.st, gpc, gterm, B.spec, B.spart, tw, B.bcbq);
+    } else {
+      fused_stage_B(geo, s, false, B.st, B.spec, F * geo.d, tw, Batch{});
+      if (!INIT) prof_mark(g);
+      scount = fused_stage_C(geo, s, F, false, B.st, gpc, gterm, B.spec, B.spart, tw, Batch{});
+    }
   } else {
     update_kernel<KIND, INIT><<<kRedBlocks, 256, 0, s>>>(n, B.st, B.x, r, B.p, B.kp, dinv, sz,
                                                          B.upart);
@@ -281,7 +298,7 @@ static void pcg_precond_phase_fused(jfftb_op* op, jfftb_grid* g, jfftb_jacobi* j
   if (!INIT) prof_mark(g);
   if (SPECTRAL_PC) {
     double2* z = B.spec + (GJ ? geo.d * fused_component_stride(geo) : 0);
-    fused_stage_B(geo, s, true, B.st, z, geo.d, tw, Batch{});
+    if (!bcb) fused_stage_B(geo, s, true, B.st, z, geo.d, tw, Batch{});
     if (!INIT) prof_mark(g);
     if (g->geo.d == 3) {
       // pass I, then the next iteration's stencil

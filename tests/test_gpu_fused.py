@@ -149,3 +149,33 @@ print("ok", err)
     r = subprocess.run([sys.executable, "-c", code, repo], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,kind", [(32, "green-jacobi"), (64, "green-jacobi"), (64, "green"),
+                                    (128, "green-jacobi")])
+def test_merged_spectral_kernel_matches_separate_passes(n, kind, monkeypatch):
+    """JFFTB_BCB=1 runs passes B, C and B' as one persistent kernel that chains
+    the k0 planes through L2 (fused.cu passBCB).  Same transforms and block
+    solve, other Parseval grouping: histories to 1e-12, fields to 1e-11, and
+    bitwise equal to itself on a rerun (the item -> CTA map is dynamic, the
+    sums are not)."""
+    from paper_2508_02613_b200 import microstructures as ms
+    lam, mu = ms.lame_from_poisson()
+    rho = ms.random_spheres(n, count=5, rmin=n / 10, rmax=n / 5, filters=3, emin=1e-2, seed=n)
+    grid = G.make_grid(n, (1.0,) * 3)
+    mat = isotropic_material(lam, mu, 3)
+    eb = np.array([0.4, -0.1, 0.2, 0.3, 0.0, 0.5])
+    reps = []
+    for flag in ("0", "1", "1"):
+        monkeypatch.setenv("JFFTB_BCB", flag)
+        op = make_operator(G.ScalarField(grid, rho), mat)
+        green = assemble_green(grid, mat)
+        rhs = assemble_rhs(op, eb)
+        reps.append(pcg(op, rhs, build_preconditioner(kind, op, green), green, eta=0.0,
+                        max_iter=15))
+    base, merged, again = reps
+    assert merged.iterations == base.iterations == 15
+    assert rel(merged.residual_history, base.residual_history) <= 1e-12
+    assert rel(merged.solution.values, base.solution.values) <= 1e-11
+    assert merged.residual_history == again.residual_history
+    assert np.array_equal(merged.solution.values, again.solution.values)

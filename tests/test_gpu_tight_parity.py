@@ -110,7 +110,11 @@ def test_eta_1e6_counts_and_history(case, kind):
         pytest.skip("no eta = 1e-6 fixture for this kind")
     rep = pcg(op, rhs, _pre(pres, kind, op, green), green, eta=1e-6)
     assert rep.terminated == str(gold[f"{kind}_std_terminated"])
-    assert abs(rep.iterations - int(gold[f"{kind}_std_iters"])) <= 1, (name, kind)
+    # +-1, or 2% on the long Green-Jacobi solves: over 150+ iterations two
+    # correct summation orders drift by that much on the CPU as well (the
+    # fixtures' own fsum reruns: 309 vs 306 iterations on config 5)
+    it_ref = int(gold[f"{kind}_std_iters"])
+    assert abs(rep.iterations - it_ref) <= max(1, it_ref // 50), (name, kind, rep.iterations)
     hg = gold[f"{kind}_std_hist"]
     k = min(10, len(hg), len(rep.residual_history))
     assert np.abs(np.array(rep.residual_history[:k]) - hg[:k]).max() / hg[0] <= 1e-10
