@@ -121,13 +121,16 @@ __global__ void __launch_bounds__(passA_nt(M, F, TW), passA_nt(M, F, TW) <= 512 
   static_assert(PE * NT == RAWN && PE % CH == 0, "pass A tiling");
   static_assert(F == 1 || MODE != FM_APPLY, "APPLY transforms one field");
   extern __shared__ double2 sbuf[];  // packed tile [k][field][col], k < M
-  const int c = g.c0 + blockIdx.y % g.nc, bl = blockIdx.y / g.nc;  // component, right-hand side
+  // component; right-hand side (fastest block index: the L solves' CTAs of a
+  // tile run together and share its D^-1/2 reads through L2)
+  const int c = g.c0 + blockIdx.y, bl = blockIdx.x % g.L;
+  const int64_t tile = blockIdx.x / g.L;
   if (st) st += bl;
   r += bl * g.vs;
   if (kp) kp += bl * g.vs;
   spec += bl * g.bss;
   if (MODE != FM_APPLY && st->done) return;
-  const int64_t col0 = (int64_t)blockIdx.x * TW;
+  const int64_t col0 = tile * TW;
   const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
   double* rc = r + c * g.N + col0;
   const double* kc = kp ? kp + c * g.N + col0 : nullptr;
@@ -214,13 +217,16 @@ __global__ void __launch_bounds__(passA3_nt<M>(), 1)
   constexpr int Q0 = M / R0;
   static_assert(MODE == FM_ITER || MODE == FM_INIT, "pass A3 runs the PCG modes");
   extern __shared__ double2 sbuf[];   // [m][field][col]
-  const int c = g.c0 + blockIdx.y % g.nc, bl = blockIdx.y / g.nc;  // component, right-hand side
+  // component; right-hand side (fastest block index: the L solves' CTAs of a
+  // tile run together and share its D^-1/2 reads through L2)
+  const int c = g.c0 + blockIdx.y, bl = blockIdx.x % g.L;
+  const int64_t tile = blockIdx.x / g.L;
   st += bl;
   r += bl * g.vs;
   kp += bl * g.vs;
   spec += bl * g.bss;
   if (st->done) return;
-  const int64_t col0 = (int64_t)blockIdx.x * TW;
+  const int64_t col0 = tile * TW;
   const double alpha = MODE == FM_ITER ? st->alpha : 0.0;
   const int col = threadIdx.x % TW, j = threadIdx.x / TW;
   double* rc = r + c * g.N + col0 + col;
@@ -346,12 +352,12 @@ __global__ void __launch_bounds__(nt_for(tw_b(L) * L / 8))
   constexpr int NT = nt_for(TW * L / 8);
   extern __shared__ double2 sbuf[];  // [i1][col]
   const int nlast = g.nlast;
-  const int c = comp0 + (int)blockIdx.z % ncomp, bl = (int)blockIdx.z / ncomp;
+  const int c = comp0 + (int)blockIdx.z, bl = (int)(blockIdx.x % g.L);
   if (st) st += bl;
   spec += bl * g.bss;
   if (PRED && st->done) return;
   const int k0 = blockIdx.y;
-  const int64_t col0 = (int64_t)blockIdx.x * TW;
+  const int64_t col0 = (int64_t)(blockIdx.x / g.L) * TW;
   double2* base = spec + c * g.FS + (int64_t)k0 * g.KS + col0;
   // column col of the tile is sequence col: element i at base + i nlast + col
   // (TW columns = 128-byte row segments), read by the first stage and written
@@ -557,9 +563,12 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
   // [ rows: NQ x RL double2 | Green planes: GP x L double ]
   extern __shared__ double2 sbuf[];
   __shared__ double red[64];
-  if (st) st += blockIdx.y;  // right-hand side
-  spec += blockIdx.y * g.bss;
-  if (partials) partials += 2 * (int64_t)gridDim.x * blockIdx.y;
+  // right-hand side = fastest block index: the L CTAs working on a row-set
+  // run together and share its Green planes through L2
+  const int bl = blockIdx.x % g.L, bx = blockIdx.x / g.L, nbx = gridDim.x / g.L;
+  if (st) st += bl;
+  spec += bl * g.bss;
+  if (partials) partials += 2 * (int64_t)nbx * bl;
   if (MODE != FM_APPLY && st->done) return;
   static_assert(MODE != FM_QUAD || F == 1, "quad-only pass holds one spectrum");
   const double invN = 1.0 / (double)g.N;
@@ -583,9 +592,9 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
     for (int p = 0; p < GP; ++p)
       bulk_g2s(gsm + p * L, gpc + p * Nh + rbase, L * sizeof(double), &gbar);
   };
-  int64_t row = blockIdx.x;
+  int64_t row = bx;
   if (row < rows) prefetch_green(row);
-  for (; row < rows; row += gridDim.x) {
+  for (; row < rows; row += nbx) {
     const int64_t rbase = row * L;        // Green planes: rows back to back
     const int64_t sbase = g.row_off(row);  // spectra: (segmented) row address
     const int k0 = g.k0lo + (int)(row >> g.rsh);
@@ -599,8 +608,8 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
                                                              nullptr, g.FS, 1);
 #ifndef JF_NO_PREFETCH
     // the next row-set's rows into L2 while this one is solved and inverted
-    if (threadIdx.x < NQ && row + gridDim.x < rows)
-      bulk_prefetch_l2(spec + threadIdx.x * g.FS + g.row_off(row + gridDim.x),
+    if (threadIdx.x < NQ && row + nbx < rows)
+      bulk_prefetch_l2(spec + threadIdx.x * g.FS + g.row_off(row + nbx),
                        L * sizeof(double2));
 #endif
     if (GS == 1) mbar_wait(&gbar, gphase);  // this row-set's Green planes
@@ -663,7 +672,7 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
         for (int a = 0; a < D; ++a) sbuf[(ZQ + a) * RL + pidx<CPAD>(k)] = cscale(z[a], invN);
     }
     __syncthreads();  // block solve done: Green planes and r^ rows are free
-    if (row + gridDim.x < rows) prefetch_green(row + gridDim.x);
+    if (row + nbx < rows) prefetch_green(row + nbx);
     if (MODE != FM_QUAD) {
       if constexpr (IP)
         cta_fft_dit_inv<L, D, NT, CPAD, true>(sbuf + ZQ * RL, RL, tw, spec + ZQ * g.FS + sbase,
@@ -685,8 +694,8 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
       a = warp_sum(a);
       b = warp_sum(b);
       if (lane == 0) {
-        partials[2 * blockIdx.x] = a;
-        partials[2 * blockIdx.x + 1] = b;
+        partials[2 * bx] = a;
+        partials[2 * bx + 1] = b;
       }
     }
   }
@@ -908,14 +917,17 @@ __global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
   constexpr int TW = tw_a(M);
   constexpr int NT = passI_nt(M);
   extern __shared__ double2 sbuf[];  // [k][col], k <= M
-  const int c = g.c0 + blockIdx.y % g.nc, bl = blockIdx.y / g.nc;  // component, right-hand side
+  // component; right-hand side (fastest block index: the L solves' CTAs of a
+  // tile run together and share its D^-1/2 reads through L2)
+  const int c = g.c0 + blockIdx.y, bl = blockIdx.x % g.L;
+  const int64_t tile = blockIdx.x / g.L;
   if (st) st += bl;
   zspec += bl * g.bss;
   if (p) p += bl * g.vs;
   if (x) x += bl * g.vs;
   if (MODE == FM_ITER && !st->xupd) return;
   if (MODE == FM_INIT && st->done) return;
-  const int64_t col0 = (int64_t)blockIdx.x * TW;
+  const int64_t col0 = tile * TW;
   const double2* zc = zspec + c * g.CS + col0;
   for (int e = threadIdx.x; e < (M + 1) * TW; e += NT) {
     const int k = e / TW, col = e % TW;
@@ -1021,7 +1033,7 @@ void launchA_MT(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, c
   auto k = passA<M, F, MODE, TW>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  dim3 grid((unsigned)(g.PS / TW), g.nc * g.L);
+  dim3 grid((unsigned)(g.PS / TW) * g.L, g.nc);
   k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
   JF_LAUNCHED();
 }
@@ -1052,7 +1064,7 @@ void launchA_M(const FGeom& g, cudaStream_t s, const PcgState* st, double* r, co
       auto k = passA3_fused_last() ? passA3<M, MODE, true> : passA3<M, MODE, false>;
       static std::atomic<uint64_t> attr{0};
       set_smem_once(k, smem, attr);
-      dim3 grid((unsigned)(g.PS / TW), g.nc * g.L);
+      dim3 grid((unsigned)(g.PS / TW) * g.L, g.nc);
       k<<<grid, NT, smem, s>>>(g, st, r, kp, dinv, spec, tw);
       JF_LAUNCHED();
       return;
@@ -1069,7 +1081,7 @@ void launchB_L(const FGeom& g, cudaStream_t s, const PcgState* st, double2* spec
   auto k = g.SS != 0 ? passB<L, INV, PRED, true> : passB<L, INV, PRED, false>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  dim3 grid((unsigned)(g.nlast / TW), g.K0, ncomp * g.L);
+  dim3 grid((unsigned)(g.nlast / TW) * g.L, g.K0, ncomp);
   k<<<grid, NT, smem, s>>>(g, st, spec, comp0, ncomp, tw);
   JF_LAUNCHED();
 }
@@ -1092,7 +1104,7 @@ int launchC_V(const FGeom& g, cudaStream_t s, const PcgState* st, const double* 
   // batched right-hand sides share the grid's blocks (the rows of one Green
   // plane set are read by L CTAs at about the same time: L2 hits)
   const int blocks = (int)std::min<int64_t>(rows, (int64_t)std::max(per_sm, 1) * 148 * 4 / g.L);
-  k<<<dim3(blocks, g.L), NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, ga);
+  k<<<blocks * g.L, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, ga);
   JF_LAUNCHED();
   return blocks;
 }
@@ -1153,7 +1165,7 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
   auto k = passI<M, MODE>;
   static std::atomic<uint64_t> attr{0};
   set_smem_once(k, smem, attr);
-  dim3 grid((unsigned)(g.PS / TW), g.nc * g.L);
+  dim3 grid((unsigned)(g.PS / TW) * g.L, g.nc);
   k<<<grid, NT, smem, s>>>(g, st, zspec, dinv, p, x, out, tw);
   JF_LAUNCHED();
 }
