@@ -195,7 +195,7 @@ PcgBuffers pcg_workspace(jfftb_grid* g, int kcount, int max_iter) {
   const bool bcb = g->fused && fused_bcb_supported(geo);
   const int sblocks = (int)std::max<int64_t>(std::max(kRedBlocks, kFusedMaxBlocks),
                                              bcb ? fused_bcb_partials(geo) : 0);
-  const size_t qbytes = sizeof(unsigned) * (2 + 2 * (size_t)(geo.n[0] / 2 + 1));
+  const size_t qbytes = sizeof(unsigned) * (2 + 3 * (size_t)(geo.n[0] / 2 + 1));
   const size_t fixed = al(sizeof(double) * n) * 3 + al(sizeof(double) * 2 * n) +
                        al(sizeof(double2) * 2 * geo.d * nspec) + al(sizeof(PcgState)) +
                        al(sizeof(double) * (kcount + 2 * sblocks + kRedBlocks)) + al(qbytes);

@@ -706,36 +706,46 @@ __global__ void __launch_bounds__(passC_nt(D, L, F), passC_minb(D, L, F, GS))
 // n1 == n2): the axis-1 transform of a k0-plane, the axis-2 transform / Green
 // block solve / inverse of its rows and the inverse axis-1 transform of its
 // z^ fields run back to back while the plane is still in L2 (one plane of
-// six fields is 24 MiB at 512^2; the 126 MB L2 holds the two or three planes
-// in flight), so the spectra cross HBM once on the way in and z^ once on the
-// way out instead of three round trips: 16.5 U of DRAM traffic instead of
-// 31.5 U for the three passes (green-jacobi, incl. 4.5 U of Green planes and
-// 3 U of write-back of the transformed r^ rows).
+// six fields is 24 MiB at 512^2; the 126 MB L2 holds the planes in flight),
+// so the spectra cross HBM once on the way in and z^ once on the way out
+// instead of three round trips: 16.5 U of DRAM traffic instead of 31.5 U for
+// the three passes (green-jacobi, incl. 4.5 U of Green planes and 3 U of
+// write-back of the transformed r^ rows).
 //
 // Work items, claimed in order from a global ticket counter by the resident
-// CTAs:  stage s = 0 .. K0 holds  C(s-1): one frequency row-set of plane
-// s-1 | B(s): one (field, 8-column tile) axis-1 transform of plane s |
-// B'(s-1): one (z^ component, tile) inverse transform of plane s-1 -- so the
-// rows B(k) writes are re-read after only B'(k-1) (24 MiB of traffic at
-// 512^2) and z^(k) after B(k+1) (48 MiB): short reuse distances for the L2.
-// C(k) waits until all B(k) items have signalled (per-plane counter,
-// release/acquire at gpu scope), B'(k) until all C(k) items have.  A waiting
-// CTA only ever waits on items with smaller tickets, which running CTAs
-// hold, so the schedule cannot deadlock whatever the residency; by the time
-// a dependent item is claimed its producers were claimed a few hundred
-// tickets earlier.  Loads of rows written during the launch go to L2 (ld.cg, fft.cuh).
-// Every C item writes its own Parseval partial pair: the sums stay in a
-// fixed order (bitwise deterministic) although the item -> CTA map is not.
+// CTAs; stage s = 0 .. K0 holds, in this order,
+//   Cr(s-1)  one r^ row-set (3 rows) of plane s-1: axis-2 transform and the
+//            termination form r^H Gt r^            (green-jacobi only)
+//   Cs(s-1)  one s^ row-set: axis-2 transform, z^ = G s^ / N, s^H G s^,
+//            inverse axis-2 transform, z^ written over s^
+//   B(s)     one (field, 8-column tile) axis-1 transform of plane s,
+//            r^ fields first
+//   B'(s-1)  one (z^ component, tile) inverse axis-1 transform of plane s-1
+// so a plane's rows are re-read after a few tens of MiB of other traffic.
+// Every item is at most 64.5 KB of shared memory and 192 threads: three fit
+// an SM.  The axis-1 transforms run in place (DIF forward, DIT inverse), so
+// between B and B' the rows of a plane sit in digit-reversed k1 order; a row
+// item looks its Green planes up at the true k1 = dif_freq(position).
+// Cr(k) / Cs(k) wait until the r^ / s^ tiles of B(k) have signalled
+// (per-plane counters, release reduction / acquire load at gpu scope), B'(k)
+// until all Cs(k) have.  A waiting CTA only ever waits on items with smaller
+// tickets, which running CTAs hold, so the schedule cannot deadlock whatever
+// the residency; by the time a dependent item is claimed its producers were
+// claimed a few hundred tickets earlier.  Rows written during the launch are
+// read with L2 loads (ld.cg).  Every row item writes its own Parseval
+// partial: the sums stay in a fixed order (bitwise deterministic) although
+// the item -> CTA map is not.
 // ---------------------------------------------------------------------------
 #ifndef JF_BCB_NT
-#define JF_BCB_NT 256
+#define JF_BCB_NT 192
 #endif
 constexpr int BCB_NT = JF_BCB_NT;
-constexpr int bcb_bufd(int L, int F) {
-  return passC_bufd(3, L, F, 1) > 2 * tw_b(L) * L ? passC_bufd(3, L, F, 1) : 2 * tw_b(L) * L;
+constexpr int bcb_bufd(int L) {  // doubles: 3 padded rows + 9 Green planes, or one tile
+  return 3 * padded_len<CPAD>(L) * 2 + 9 * L > 2 * tw_b(L) * L ? 3 * padded_len<CPAD>(L) * 2 + 9 * L
+                                                                : 2 * tw_b(L) * L;
 }
-constexpr int bcb_minb(int L, int F) {
-  return bcb_bufd(L, F) * 8 <= 110 * 1024 ? 2 : 1;
+constexpr int bcb_minb(int L) {
+  return bcb_bufd(L) * 8 <= 72 * 1024 ? 3 : (bcb_bufd(L) * 8 <= 110 * 1024 ? 2 : 1);
 }
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -743,40 +753,109 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
+// one in-place stage of the axis-1 transform of a [L][TW] tile (element e of
+// column q at buf[e * TW + q], in global memory at base + e * gks + q;
+// consecutive threads take consecutive columns: 128-byte row segments).
+// Forward DIF: stage 0 reads global, the last stage writes global; inverse
+// DIT: stage nstages-1 reads global, stage 0 writes global.
+template <int L, int TW, int NT, bool INV, int S>
+__device__ __forceinline__ void tile_ip_stage(double2* buf, const double2* __restrict__ tw,
+                                              double2* base, int64_t gks) {
+  constexpr int NS = fft_nstages(L);
+  constexpr int R = fft_radix(L, S);
+  constexpr int P = fft_span(L, S);
+  constexpr int Q = P / R;
+  constexpr int B = TW * (L / R);
+  constexpr bool FIRST = INV ? S == NS - 1 : S == 0;  // reads global
+  constexpr bool LAST = INV ? S == 0 : S == NS - 1;   // writes global
+  const double2* __restrict__ tws = tw + tw_stage_off(P, R);
+#pragma unroll 1
+  for (int b = threadIdx.x; b < B; b += NT) {
+    const int q = b % TW, bb = b / TW;
+    const int j = bb % Q;
+    const int e0 = (bb / Q) * P + j;
+    double2 v[8];
+    if constexpr (FIRST) {
+#pragma unroll
+      for (int t = 0; t < R; ++t) v[t] = __ldcg(base + (int64_t)(e0 + Q * t) * gks + q);
+    } else {
+#pragma unroll
+      for (int t = 0; t < R; ++t) v[t] = buf[(e0 + Q * t) * TW + q];
+    }
+    if (INV && Q > 1) {
+#pragma unroll
+      for (int t = 1; t < R; ++t) v[t] = cmulc(v[t], __ldg(tws + (t - 1) * Q + j));
+    }
+    dftR<R, INV>(v);
+    if (!INV && Q > 1) {
+#pragma unroll
+      for (int t = 1; t < R; ++t) v[t] = cmul(v[t], __ldg(tws + (t - 1) * Q + j));
+    }
+    if constexpr (LAST) {
+#pragma unroll
+      for (int t = 0; t < R; ++t) base[(int64_t)(e0 + Q * t) * gks + q] = v[t];
+    } else {
+#pragma unroll
+      for (int t = 0; t < R; ++t) buf[(e0 + Q * t) * TW + q] = v[t];
+    }
+  }
+  if constexpr (!LAST) __syncthreads();
+}
+template <int L, int TW, int NT, int S = 0>
+__device__ __forceinline__ void tile_fft_dif(double2* buf, const double2* __restrict__ tw,
+                                             double2* base, int64_t gks) {
+  if constexpr (S < fft_nstages(L)) {
+    tile_ip_stage<L, TW, NT, false, S>(buf, tw, base, gks);
+    tile_fft_dif<L, TW, NT, S + 1>(buf, tw, base, gks);
+  }
+}
+template <int L, int TW, int NT, int S = fft_nstages(L) - 1>
+__device__ __forceinline__ void tile_fft_dit_inv(double2* buf, const double2* __restrict__ tw,
+                                                 double2* base, int64_t gks) {
+  if constexpr (S >= 0) {
+    tile_ip_stage<L, TW, NT, true, S>(buf, tw, base, gks);
+    tile_fft_dit_inv<L, TW, NT, S - 1>(buf, tw, base, gks);
+  }
+}
+
 template <int L, int F>
-__global__ void __launch_bounds__(BCB_NT, bcb_minb(L, F))
+__global__ void __launch_bounds__(BCB_NT, bcb_minb(L))
     passBCB(FGeom g, const PcgState* __restrict__ st, const double* __restrict__ gpc,
             const double* __restrict__ gterm, double2* __restrict__ spec,
             double* __restrict__ partials, const double2* __restrict__ tw,
             unsigned* __restrict__ q) {
-  constexpr int D = 3, NQ = F * D, NT = BCB_NT;
+  constexpr int D = 3, NT = BCB_NT;
   constexpr int TW = tw_b(L), NTILE = L / TW;
   constexpr int RL = padded_len<CPAD>(L);
-  constexpr int GP = passC_gp(D, 1);
-  constexpr int ZQ = F == 2 ? D : 0;
+  constexpr int GP = 9;
+  constexpr int ZQ = F == 2 ? D : 0;  // first field of the solved spectrum
+  static_assert(fft_nstages(L) >= 2, "axis-1 tiles need two stages");
   extern __shared__ double2 sbuf[];
-  __shared__ double red[64];
+  __shared__ double red[32];
   __shared__ uint64_t gbar;
   __shared__ unsigned s_ticket;
   if (st->done) return;
   const int K = g.K0;
-  const unsigned nB = NQ * NTILE, nC = (unsigned)(g.PS / L), nBi = D * NTILE;
-  const unsigned per = nB + nC + nBi, total = (unsigned)(K + 1) * per;
-  unsigned* cntB = q + 2;
-  unsigned* cntC = cntB + K;
+  const unsigned nR = (unsigned)(g.PS / L);          // rows of a plane
+  const unsigned nCr = F == 2 ? nR : 0, nCs = nR;
+  const unsigned nB = F * D * NTILE, nBi = D * NTILE;
+  const unsigned per = nCr + nCs + nB + nBi, total = (unsigned)(K + 1) * per;
+  unsigned* cntBr = q + 2;      // r^ tiles of plane k transformed (F = 2)
+  unsigned* cntBs = cntBr + K;  // tiles of the solved fields transformed
+  unsigned* cntC = cntBs + K;   // solved row-sets of plane k written
   const double invN = 1.0 / (double)g.N;
   const int64_t Nh = g.CS;
-  double* gsm = reinterpret_cast<double*>(sbuf + NQ * RL);
+  double* gsm = reinterpret_cast<double*>(sbuf + D * RL);
   unsigned gphase = 0;
   if (threadIdx.x == 0) mbar_init(&gbar, 1);
-  // all of a producer item's stores, then (thread 0) fence + count
-  // (a release reduction: nobody waits for its round trip)
+  // all of a producer item's stores, then (thread 0) a release reduction:
+  // nobody waits for its round trip
   auto signal = [&](unsigned* cnt) {
     __syncthreads();
     if (threadIdx.x == 0)
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(cnt) : "memory");
   };
-  // returns false if the producers never arrive (a bug guard, not a path)
+  // (the spin bound is a bug guard, not a path: q[1] reports it)
   auto wait_for = [&](const unsigned* cnt, unsigned need) {
     if (threadIdx.x == 0) {
       unsigned spins = 0;
@@ -790,109 +869,121 @@ __global__ void __launch_bounds__(BCB_NT, bcb_minb(L, F))
     }
     __syncthreads();
   };
+  // the Green planes of frequency row (k, k1) -> shared memory (bulk copies)
+  auto fetch_green = [&](const double* gp, int64_t grow) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async();  // earlier generic accesses of the buffer come first
+      mbar_expect_tx(&gbar, GP * L * sizeof(double));
+#pragma unroll 1
+      for (int p = 0; p < GP; ++p)
+        bulk_g2s(gsm + p * L, gp + p * Nh + grow * L, L * sizeof(double), &gbar);
+    }
+  };
+  auto load_block = [&](int kk) {
+    HB<D> B;
+#pragma unroll
+    for (int a = 0; a < D; ++a) B.dg[a] = gsm[a * L + kk];
+#pragma unroll
+    for (int oo = 0; oo < 3; ++oo) {
+      B.re[oo] = gsm[(D + 2 * oo) * L + kk];
+      B.im[oo] = gsm[(D + 2 * oo + 1) * L + kk];
+    }
+    return B;
+  };
+  // fixed-order block sum (warp tree, then warps in order) -> *out by thread 0
+  auto block_partial = [&](double v, double* out) {
+    v = warp_sum(v * invN);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+#pragma unroll
+      for (int i = 0; i < NT / 32; ++i) a += red[i];
+      *out = a;
+    }
+  };
   // the next ticket is drawn while the current item runs
   unsigned next = 0;
   if (threadIdx.x == 0) next = atomicAdd(q, 1u);
   for (;;) {
-    __syncthreads();  // the previous item is done with s_ticket and the tile
+    __syncthreads();  // the previous item is done with s_ticket and the buffer
     if (threadIdx.x == 0) s_ticket = next;
     __syncthreads();
     const unsigned t = s_ticket;
     if (t >= total) break;
     if (threadIdx.x == 0) next = atomicAdd(q, 1u);
     const int s = (int)(t / per);
-    const unsigned o = t % per;
-    if (o >= nC && o < nC + nB) {
-      // ---- B(s): axis-1 transform of (field c, column tile) of plane s
-      const int k = s;
-      if (k >= K) continue;
-      const unsigned ob = o - nC;
-      const int c = (int)(ob / NTILE), tile = (int)(ob % NTILE);
-      double2* base = spec + c * g.FS + (int64_t)k * g.KS + (int64_t)tile * TW;
-      cta_fft_io<L, TW, NT, false, true, 0, true, true, false>(sbuf, TW, 1, tw, base, base, 1,
-                                                               g.nlast);
-      signal(cntB + k);
-    } else if (o < nC) {
-      // ---- C(s-1): one frequency row-set (F * 3 rows) of plane s - 1
+    unsigned o = t % per;
+    if (o < nCr + nCs) {
+      // ---- a row-set of plane s - 1 (position pr along axis 1 holds k1)
       const int k = s - 1;
-      if (k < 0 || k >= K) continue;
-      const int64_t row = (int64_t)k * nC + o;
-      const int64_t rbase = row * L;
+      if (k < 0) continue;
+      const bool solve = o >= nCr;  // Cs; else Cr (termination form only)
+      const unsigned pr = solve ? o - nCr : o;
+      const int k1 = dif_freq(L, (int)pr);
+      const int64_t row = (int64_t)k * nR + pr;
       const int k0 = g.k0lo + k;
       const double w = (k0 == 0 || 2 * k0 == g.n0) ? 1.0 : 2.0;
-      if (threadIdx.x == 0) {
-        fence_proxy_async();  // earlier generic accesses of the tile come first
-        mbar_expect_tx(&gbar, GP * L * sizeof(double));
-#pragma unroll 1
-        for (int p = 0; p < GP; ++p)
-          bulk_g2s(gsm + p * L, gpc + p * Nh + rbase, L * sizeof(double), &gbar);
-      }
-      wait_for(cntB + k, nB);
-      cta_fft_dif<L, NQ, NT, CPAD, true>(sbuf, RL, tw, spec + rbase, g.FS);
+      const int fq = solve ? ZQ : 0;  // first field of the row-set
+      fetch_green(solve ? gpc : gterm, (int64_t)k * nR + k1);
+      wait_for((solve || F == 1) ? cntBs + k : cntBr + k, D * NTILE);
+      cta_fft_dif<L, D, NT, CPAD, true>(sbuf, RL, tw, spec + fq * g.FS + row * L, g.FS);
       mbar_wait(&gbar, gphase);
       gphase ^= 1;
       double q0 = 0.0, q1 = 0.0;
 #pragma unroll 1
       for (int kk = threadIdx.x; kk < L; kk += NT) {
-        const int64_t f = rbase + kk;
-        HB<D> B;
-#pragma unroll
-        for (int a = 0; a < D; ++a) B.dg[a] = gsm[a * L + kk];
-#pragma unroll
-        for (int oo = 0; oo < 3; ++oo) {
-          B.re[oo] = gsm[(D + 2 * oo) * L + kk];
-          B.im[oo] = gsm[(D + 2 * oo + 1) * L + kk];
-        }
+        const HB<D> B = load_block(kk);
         double2 sv[D], z[D];
 #pragma unroll
-        for (int a = 0; a < D; ++a) sv[a] = sbuf[(ZQ + a) * RL + pidx<CPAD>(kk)];
+        for (int a = 0; a < D; ++a) sv[a] = sbuf[a * RL + pidx<CPAD>(kk)];
         const double qs = hb_apply<D>(B, sv, z);
-        if (F == 2) {
-          double2 rr[D], tmp[D];
-#pragma unroll
-          for (int a = 0; a < D; ++a) rr[a] = sbuf[a * RL + pidx<CPAD>(kk)];
-          const double qr = (gterm == gpc) ? hb_apply<D>(B, rr, tmp)
-                                           : hb_apply<D>(ld_block<D>(gterm, Nh, f), rr, tmp);
-          q0 += w * qr;
-          q1 += w * qs;
+        if (!solve) {
+          q0 += w * qs;
         } else {
           q1 += w * qs;
-          if (gterm == gpc) {
-            q0 += w * qs;
-          } else {
-            double2 tmp[D];
-            q0 += w * hb_apply<D>(ld_block<D>(gterm, Nh, f), sv, tmp);
+          if (F == 1) {
+            if (gterm == gpc) {
+              q0 += w * qs;
+            } else {
+              double2 tmp[D];
+              q0 += w * hb_apply<D>(ld_block<D>(gterm, Nh, ((int64_t)k * nR + k1) * L + kk), sv,
+                                    tmp);
+            }
           }
+#pragma unroll
+          for (int a = 0; a < D; ++a) sbuf[a * RL + pidx<CPAD>(kk)] = cscale(z[a], invN);
         }
-#pragma unroll
-        for (int a = 0; a < D; ++a) sbuf[(ZQ + a) * RL + pidx<CPAD>(kk)] = cscale(z[a], invN);
       }
-      // this row-set's Parseval pair (fixed order: warp tree, then warps 0..7)
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-      q0 = warp_sum(q0 * invN);
-      q1 = warp_sum(q1 * invN);
-      if (lane == 0) { red[wid] = q0; red[32 + wid] = q1; }
-      __syncthreads();  // block solve done: z^ rows complete, partials staged
-      if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-#pragma unroll
-        for (int i = 0; i < NT / 32; ++i) { a += red[i]; b += red[32 + i]; }
-        partials[2 * row] = a;
-        partials[2 * row + 1] = b;
+      if (!solve) {
+        block_partial(q0, partials + 2 * row);
+      } else {
+        if (F == 1) {
+          block_partial(q0, partials + 2 * row);
+          __syncthreads();  // red is reused
+        }
+        block_partial(q1, partials + 2 * row + 1);  // (its barrier: z^ rows complete)
+        cta_fft_dit_inv<L, D, NT, CPAD, true>(sbuf, RL, tw, spec + ZQ * g.FS + row * L, g.FS);
+        signal(cntC + k);
       }
-      cta_fft_dit_inv<L, D, NT, CPAD, true>(sbuf + ZQ * RL, RL, tw, spec + ZQ * g.FS + rbase,
-                                            g.FS);
-      signal(cntC + k);
+    } else if (o < nCr + nCs + nB) {
+      // ---- B(s): axis-1 transform of (field c, column tile) of plane s
+      const int k = s;
+      if (k >= K) continue;
+      o -= nCr + nCs;
+      const int c = (int)(o / NTILE), tile = (int)(o % NTILE);
+      double2* base = spec + c * g.FS + (int64_t)k * g.KS + (int64_t)tile * TW;
+      tile_fft_dif<L, TW, NT>(sbuf, tw, base, g.nlast);
+      signal((F == 2 && c < D) ? cntBr + k : cntBs + k);
     } else {
       // ---- B'(s-1): inverse axis-1 transform of (z^ component, tile) of plane s - 1
       const int k = s - 1;
-      if (k < 0 || k >= K) continue;
-      const unsigned oo = o - nB - nC;
-      const int c = ZQ + (int)(oo / NTILE), tile = (int)(oo % NTILE);
-      wait_for(cntC + k, nC);
+      if (k < 0) continue;
+      o -= nCr + nCs + nB;
+      const int c = ZQ + (int)(o / NTILE), tile = (int)(o % NTILE);
+      wait_for(cntC + k, nR);
       double2* base = spec + c * g.FS + (int64_t)k * g.KS + (int64_t)tile * TW;
-      cta_fft_io<L, TW, NT, true, true, 0, true, true, false>(sbuf, TW, 1, tw, base, base, 1,
-                                                              g.nlast);
+      tile_fft_dit_inv<L, TW, NT>(sbuf, tw, base, g.nlast);
     }
   }
 }
@@ -1138,7 +1229,7 @@ int launchBCB_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double
                 const double* gterm, double2* spec, double* partials, const double2* tw,
                 unsigned* q) {
   constexpr int NT = BCB_NT;
-  const size_t smem = sizeof(double) * bcb_bufd(L, F);
+  const size_t smem = sizeof(double) * bcb_bufd(L);
   auto k = passBCB<L, F>;
   static std::atomic<uint64_t> attr{0};
   static int per_sm_dev[64];
@@ -1150,7 +1241,7 @@ int launchBCB_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double
   int sms = 0;
   JF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int blocks = std::max(per_sm_dev[dev], 1) * sms;
-  JF_CUDA(cudaMemsetAsync(q, 0, sizeof(unsigned) * (2 + 2 * (size_t)g.K0), s));
+  JF_CUDA(cudaMemsetAsync(q, 0, sizeof(unsigned) * (2 + 3 * (size_t)g.K0), s));
   k<<<blocks, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, q);
   JF_LAUNCHED();
   return (int)(g.CS / L);
@@ -1362,10 +1453,9 @@ int fused_stage_C(const Geom& geo, cudaStream_t s, int F, bool quad_only, const 
 }
 // Merged B / C / B' (passBCB): 3-D grids with n1 == n2, one solve, stored
 // Green planes.  Opt-in (JFFTB_BCB=1): it halves the DRAM traffic of the three
-// passes (ncu, 512^3 green-jacobi: 18.0 GB vs 33.8 GB per iteration) but runs
-// slower than them (7.9 vs 6.5 ms): with 92 KB of shared memory and 128
-// registers x 256 threads per item only two items fit an SM, and the items
-// are latency-bound (B 6.3 us, C 9.0 us, B' 5.0 us each), while the separate
+// passes (ncu, 512^3 green-jacobi: 18.2 GB vs 33.8 GB per iteration) but runs
+// slower than them (7.5 vs 6.5 ms): three items fit an SM and an item is a
+// serial chain of barrier-separated stages (~8 us), while the separate
 // passes each fill the SM for their own bottleneck (profiles/r02_ab_notes.md)
 bool fused_bcb_supported(const Geom& geo) {
   const char* e = std::getenv("JFFTB_BCB");  // read per solve (tests switch it)
@@ -1376,7 +1466,7 @@ bool fused_bcb_supported(const Geom& geo) {
 int64_t fused_bcb_partials(const Geom& geo) {
   return geo.d == 3 ? (int64_t)(geo.n[0] / 2 + 1) * geo.n[1] : 0;
 }
-// returns the number of partial pairs written; q: 2 + 2 K0 counters
+// returns the number of partial pairs written; q: 2 + 3 K0 counters
 int fused_stage_BCB(const Geom& geo, cudaStream_t s, int F, const PcgState* st,
                     const jfftb_green* gpc_h, const jfftb_green* gterm_h, double2* spec,
                     double* partials, const double2* tw, unsigned* q) {
