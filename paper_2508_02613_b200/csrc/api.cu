@@ -1014,6 +1014,7 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     const int kcount = stencil_blocks(geo);
     PcgBuffers B = pcg_workspace(g, kcount, max_iter);
     PcgState* hs = g->ws_host;
+    if (B.bcbq) JF_CUDA(cudaMemsetAsync(B.bcbq, 0, 2 * sizeof(unsigned), s));
 
     // fault in a pageable solution array on host threads while the device
     // iterates, so the final d2h is a plain staged memcpy
@@ -1063,7 +1064,12 @@ int jfftb_pcg(jfftb_op* op, int kind, jfftb_green* green_pc, jfftb_jacobi* jac,
     *iterations = it;
     JF_CUDA(cudaMemcpyAsync(history_out, B.hist, sizeof(double) * (it + 1),
                             cudaMemcpyDeviceToHost, s));
+    unsigned bcb_flag = 0;
+    if (B.bcbq)
+      JF_CUDA(cudaMemcpyAsync(&bcb_flag, B.bcbq + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     JF_CUDA(cudaStreamSynchronize(s));
+    if (bcb_flag)
+      throw Error(JFFTB_ECUDA, "merged spectral pass: a work item's producers never arrived");
     if (hs->status != JFFTB_OK) {
       if (wall_s)
         *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -1241,7 +1241,10 @@ int launchBCB_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double
   int sms = 0;
   JF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int blocks = std::max(per_sm_dev[dev], 1) * sms;
-  JF_CUDA(cudaMemsetAsync(q, 0, sizeof(unsigned) * (2 + 3 * (size_t)g.K0), s));
+  // q[0]: ticket counter, q[1]: sticky wait-timeout flag (cleared and checked
+  // by jfftb_pcg), q[2 ...]: per-plane counters
+  JF_CUDA(cudaMemsetAsync(q, 0, sizeof(unsigned), s));
+  JF_CUDA(cudaMemsetAsync(q + 2, 0, sizeof(unsigned) * 3 * (size_t)g.K0, s));
   k<<<blocks, NT, smem, s>>>(g, st, gpc, gterm, spec, partials, tw, q);
   JF_LAUNCHED();
   return (int)(g.CS / L);
