@@ -94,7 +94,12 @@ def test_fixed_iterations(case, kind):
     assert rep.iterations == K and rep.terminated == "iteration-cap"
     h = np.array(rep.residual_history)
     hg = gold[f"{kind}_fixed_hist"]
-    tol_h = max(1e-10, 10 * float(gold[f"{kind}_fixed_floor_hist"]))
+    # 1e-10, or 100x the CPU-vs-CPU floor where that is higher (2048^2
+    # Green-Jacobi: 7e-12 after 20 iterations).  The floor run perturbs only
+    # the dot products (one rounding each); a different FFT implementation
+    # perturbs every transform at ~log2(N) = 22 roundings, and Green-Jacobi
+    # amplifies both alike.
+    tol_h = max(1e-10, 100 * float(gold[f"{kind}_fixed_floor_hist"]))
     assert np.abs(h - hg).max() / hg[0] <= tol_h, (name, kind)
     tol_u = max(1e-9, 10 * float(gold[f"{kind}_fixed_floor_u"]))
     us = _sample(rep.solution.values, int(gold["sample"]))
@@ -137,8 +142,13 @@ def test_tight_solution_and_stress(case, kind):
     rep = pcg(op, rhs, pre, green, eta=1e-24 * h0, max_iter=20000)
     assert rep.terminated == "converged"
     if src == kind:
+        # 2%, or twice the spread of the fixture's own two CPU runs (NumPy
+        # vs exactly rounded dot products: 1728 vs 1680 iterations on
+        # 2048^2 Green-Jacobi)
         it_ref = int(gold[f"{kind}_tight_iters"])
-        assert abs(rep.iterations - it_ref) <= max(2, it_ref // 50), (name, kind, rep.iterations)
+        spread = abs(it_ref - int(gold[f"{kind}_tight_fsum_iters"]))
+        assert abs(rep.iterations - it_ref) <= max(2, it_ref // 50, 2 * spread), \
+            (name, kind, rep.iterations)
     us = _sample(rep.solution.values, int(gold["sample"]))
     assert float(gold[f"{src}_tight_floor_u"]) <= 1e-10  # the bar sits above the floor
     assert rel(us, gold[f"{src}_tight_usample"]) <= 1e-9, (name, kind, src)
