@@ -110,7 +110,8 @@ constexpr int passA_nt(int M, int F, int TW) {
 }
 
 template <int M, int F, int MODE, int TW>
-__global__ void __launch_bounds__(passA_nt(M, F, TW), passA_nt(M, F, TW) <= 512 ? 2 : 1)
+__global__ void __launch_bounds__(passA_nt(M, F, TW),
+                                  passA_nt(M, F, TW) <= 512 && 16 * F * TW * M <= 110 * 1024 ? 2 : 1)
     passA(FGeom g, const PcgState* __restrict__ st, double* __restrict__ r,
           const double* __restrict__ kp, const double* __restrict__ dinv,
           double2* __restrict__ spec, const double2* __restrict__ tw) {
@@ -994,10 +995,23 @@ __global__ void __launch_bounds__(BCB_NT, bcb_minb(L))
 //   FM_INIT:  p = Dz
 //   FM_APPLY: out = Dz           (D = D^-1/2 for green-jacobi, identity for green)
 // ---------------------------------------------------------------------------
-constexpr int passI_nt(int M) { return nt_for(tw_a(M) * M / 4); }
+// pass I tile width (columns): its tile holds one field, so at M = 512
+// (n0 = 1024: the per-rank slabs of the 1024^3 multi-GPU configuration) it
+// keeps 16 columns (128-byte row segments, one 131 KB tile per SM) where pass
+// A's two-field tile only fits 8 -- measured on a (1024, 256, 512) grid: pass
+// I 5.57 -> 3.86 ms, the iteration 21.07 -> 20.02 ms; at M = 1024 (2-D
+// 2048^2) 8 columns measured no better than 4
+#ifndef JF_TWI_512
+#define JF_TWI_512 16
+#endif
+#ifndef JF_TWI_1024
+#define JF_TWI_1024 4
+#endif
+constexpr int tw_i(int M) { return M >= 1024 ? JF_TWI_1024 : (M >= 512 ? JF_TWI_512 : 16); }
+constexpr int passI_nt(int M) { return nt_for(tw_i(M) * M / 4); }
 // two resident CTAs per SM where the tile fits twice (register cap 64)
 constexpr int passI_minb(int M) {
-  return 2 * (size_t)16 * tw_a(M) * (M + 1) <= 200 * 1024 && passI_nt(M) >= 512 ? 2 : 1;
+  return 2 * (size_t)16 * tw_i(M) * (M + 1) <= 200 * 1024 && passI_nt(M) >= 512 ? 2 : 1;
 }
 
 template <int M, int MODE>
@@ -1005,7 +1019,7 @@ __global__ void __launch_bounds__(passI_nt(M), passI_minb(M))
     passI(FGeom g, const PcgState* __restrict__ st, const double2* __restrict__ zspec,
           const double* __restrict__ dinv, double* __restrict__ p, double* __restrict__ x,
           double* __restrict__ out, const double2* __restrict__ tw) {
-  constexpr int TW = tw_a(M);
+  constexpr int TW = tw_i(M);
   constexpr int NT = passI_nt(M);
   extern __shared__ double2 sbuf[];  // [k][col], k <= M
   // component; right-hand side (fastest block index: the L solves' CTAs of a
@@ -1253,7 +1267,7 @@ int launchBCB_L(const FGeom& g, cudaStream_t s, const PcgState* st, const double
 template <int M, int MODE>
 void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2* zspec,
                const double* dinv, double* p, double* x, double* out, const double2* tw) {
-  constexpr int TW = tw_a(M);
+  constexpr int TW = tw_i(M);
   constexpr int NT = passI_nt(M);
   const size_t smem = sizeof(double2) * TW * (M + 1);
   auto k = passI<M, MODE>;
@@ -1264,11 +1278,14 @@ void launchI_M(const FGeom& g, cudaStream_t s, const PcgState* st, const double2
   JF_LAUNCHED();
 }
 
-#ifdef JF_FAST_BUILD  // A/B builds: the 128 and 512 instantiations only
+#ifdef JF_FAST_BUILD  // A/B builds: fewer instantiations
 #define JF_SIZE_SWITCH(L, CALL)                   \
   switch (L) {                                    \
     case 128: { constexpr int LL = 128; CALL; break; } \
+    case 256: { constexpr int LL = 256; CALL; break; } \
     case 512: { constexpr int LL = 512; CALL; break; } \
+    case 1024: { constexpr int LL = 1024; CALL; break; } \
+    case 2048: { constexpr int LL = 2048; CALL; break; } \
     default: throw Error(JFFTB_EINVAL, "fused FFT: unsupported size (fast build)"); \
   }
 #else
