@@ -85,7 +85,10 @@ struct FGeom {
 };
 
 constexpr int tw_a(int M) { return M >= 1024 ? 4 : (M >= 512 ? 8 : 16); }
-constexpr int tw_b(int L) { return L >= 1024 ? 4 : 8; }
+#ifndef JF_TWB_1024
+#define JF_TWB_1024 4
+#endif
+constexpr int tw_b(int L) { return L >= 2048 ? 4 : (L >= 1024 ? JF_TWB_1024 : 8); }
 // one radix-8 butterfly per thread where possible (<= 512 threads)
 constexpr int nt_for(int butterflies) {
   return butterflies >= 512 ? 512 : (butterflies <= 64 ? 64 : (butterflies + 31) / 32 * 32);
