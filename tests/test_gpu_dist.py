@@ -123,6 +123,33 @@ def test_loopback_vs_oracle_fixed_iterations():
     assert rel(glob(rep.solution, P), x) <= 1e-10
 
 
+@pytest.mark.parametrize("shape,P", [((32, 64, 32), 2), ((32, 64, 64), 4)])
+def test_loopback_weak_scaled_cells_vs_oracle(shape, P):
+    """The non-cubic cells bench.py --gpus 2 / 4 solve (axes 1 and 2 doubled,
+    same pixel size) against the oracle: the first 10 Green-Jacobi iterates."""
+    lengths = tuple(k / 32 for k in shape)
+    rng = np.random.default_rng(21)
+    rho = 0.05 + rng.random(shape)
+    for _ in range(2):  # a little smoothing keeps the contrast moderate
+        rho = 0.5 * rho + 0.25 * (np.roll(rho, 1, 1) + np.roll(rho, -1, 2))
+    eb = ms.mandel_shear(3, 0, 2, 0.5)
+    c = X.isotropic_stiffness(3, LAM, MU)
+    h = X.pixel_size(shape, lengths)
+    blocks = X.assemble_green(shape, lengths, c)
+    inv = X.assemble_jacobi(rho, c, h)
+    f = X.assemble_rhs(rho, c, h, eb)
+    it, hist, term, x = X.pcg(rho, c, h, f, "green-jacobi", blocks, inv, eta=0.0, max_iter=10)
+    comm = Dm.Comm.local_ranks(P)
+    D = Dm.DistSolver(comm, shape, lengths, np.stack(Dm.split(rho, P, axis=1)), LAM, MU,
+                      kind="green-jacobi")
+    rhs = D.assemble_rhs(eb)
+    assert rel(glob(rhs, P), f) <= 1e-13
+    rep = D.pcg(rhs, eta=0.0, max_iter=10)
+    assert rep.iterations == it == 10
+    assert rel(rep.residual_history, hist) <= 1e-11
+    assert rel(glob(rep.solution, P), x) <= 1e-10
+
+
 @pytest.mark.parametrize("kind", ["green-jacobi", "green"])
 def test_pipelined_exchange_bitwise(kind, monkeypatch):
     """The per-component pipelined all-to-alls (exchange stream + events,
