@@ -365,3 +365,39 @@ def test_uniform_medium_one_iteration():
         sig = homogenized_stress(op, G.VectorField.zeros(grid), eb)
         c = X.isotropic_stiffness(d, 2.0 / 3.0, 0.5)
         assert np.allclose(sig, c @ eb, rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("d,n", [(3, 48), (3, 24), (2, 96), (2, 40)])
+@pytest.mark.parametrize("kind", KINDS)
+def test_non_power_of_two_grids_match_oracle(d, n, kind):
+    """Grids that are not powers of two run the library's cuFFT path (same
+    stencil, Green setup, block solve and reductions): the
+    first 12 iterates of every preconditioner kind against the oracle, and the
+    converged solve's iteration count."""
+    lam, mu = ms.lame_from_poisson()
+    rng = np.random.default_rng(1000 * d + n)
+    rho = 1e-3 + rng.random((n,) * d) ** 3  # rough, contrast ~500
+    rho = 0.5 * rho + 0.5 * np.roll(rho, 1, 0)
+    lengths = (1.0,) * d
+    eb = ms.mandel_shear(d, 0, d - 1, 0.5)
+    c = X.isotropic_stiffness(d, lam, mu)
+    h = X.pixel_size((n,) * d, lengths)
+    blocks = X.assemble_green((n,) * d, lengths, c)
+    inv = X.assemble_jacobi(rho, c, h)
+    f = X.assemble_rhs(rho, c, h, eb)
+    grid = G.make_grid(n, lengths)
+    mat = isotropic_material(lam, mu, d)
+    op = make_operator(G.ScalarField(grid, rho), mat)
+    green = assemble_green(grid, mat)
+    rhs = assemble_rhs(op, eb)
+    assert rel(rhs.values, f) <= 1e-13
+    pre = build_preconditioner(kind, op, green)
+    it, hist, term, x = X.pcg(rho, c, h, f, kind, blocks, inv, eta=0.0, max_iter=12)
+    rep = pcg(op, rhs, pre, green, eta=0.0, max_iter=12)
+    assert rep.iterations == it == 12 and rep.terminated == ITERATION_CAP
+    assert rel(rep.residual_history, hist) <= 1e-11
+    assert rel(rep.solution.values, x) <= 1e-10
+    it, hist, term, x = X.pcg(rho, c, h, f, kind, blocks, inv, eta=1e-8, max_iter=400)
+    rep = pcg(op, rhs, pre, green, eta=1e-8, max_iter=400)
+    assert rep.terminated == (CONVERGED if term == X.CONVERGED else ITERATION_CAP)
+    assert abs(rep.iterations - it) <= max(1, it // 50)
